@@ -1,0 +1,134 @@
+/*
+ * gpp_b200.h -- C ABI of the B200-native GPP self-energy library
+ * (libgpp_b200.so, built from paper_2008_11326_b200/csrc/).
+ *
+ * The reference (`rooflab`, pure Python) has no FFI: its drop-in seam is the
+ * Python function
+ *     evaluate_variant(problem: GPPProblem, variant: str) -> GPPResult
+ *         rooflab/gpp/kernel.py:98-114
+ * called by run_version (rooflab/gpp/runner.py:249-286), with the oracle
+ * reference_result (rooflab/gpp/problem.py:179-208) and the branch
+ * statistics branch_stats (rooflab/gpp/kernel.py:130-137) beside it.
+ * This header is the boundary those calls cross on the B200 path; the
+ * ctypes shim paper_2008_11326_b200/_lib.py binds every entry point below,
+ * and INTEGRATION.md shows the binding a rooflab maintainer would add.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Complex arrays are interleaved
+ *     (re, im) float64, column-major (Fortran order) exactly as numpy holds
+ *     the reference's GPPProblem arrays (problem.py:50-61).
+ *   - Every int-returning call returns a GPP_* status; on failure
+ *     gpp_last_error() returns a thread-local message.
+ *   - Host input buffers are borrowed for the duration of the call only and
+ *     never written.  Outputs go to caller-allocated host buffers.
+ *   - A gpp_ctx is single-caller (not thread-safe); distinct contexts may be
+ *     used concurrently (the reference allows concurrent independent runs,
+ *     SPEC.md:412).
+ *   - There is no CPU fallback: without a working CUDA device every compute
+ *     entry point fails with GPP_ERR_CUDA.
+ */
+#ifndef GPP_B200_H
+#define GPP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GPP_ABI_VERSION 1
+
+/* Status codes.  The shim raises GPP_ERR_ARG as DomainError and the others as
+ * GPUError; both derive from RooflabError (rooflab/errors.py:8-21), so the
+ * reference CLI's exit-1 mapping (rooflab/cli.py:341-343) is preserved. */
+#define GPP_OK 0
+#define GPP_ERR_ARG 1
+#define GPP_ERR_CUDA 2
+#define GPP_ERR_NCCL 3
+#define GPP_ERR_OOM 4
+
+/* Arithmetic variants, rooflab/gpp/kernel.py:30 VARIANTS = (div, rcp, rcp_sq).
+ * DIV and RCP evaluate the per-instance formulas as the reference writes them
+ * (kernel.py:68-95, IEEE division and sqrt); RCP_SQ is the optimised
+ * squared-magnitude / reciprocal-multiply kernel (the paper's v8). */
+#define GPP_VARIANT_DIV 0
+#define GPP_VARIANT_RCP 1
+#define GPP_VARIANT_RCP_SQ 2
+
+typedef struct gpp_ctx gpp_ctx;
+
+/* ABI revision (GPP_ABI_VERSION) of the loaded library. */
+int gpp_abi_version(void);
+
+/* Thread-local message describing the last failure on this thread. */
+const char* gpp_last_error(void);
+
+/* Number of visible CUDA devices. */
+int gpp_device_count(int* count);
+
+/* Create a context bound to one CUDA device.  Lazy: no CUDA call is made
+ * until the first upload, so argument validation works without a GPU. */
+int gpp_create(gpp_ctx** ctx, int device);
+void gpp_destroy(gpp_ctx* ctx);
+
+/* Copy one problem (or the band shard [band0, band1) of it) to the device.
+ * Replaces the array hand-off into evaluate_variant (kernel.py:98) and the
+ * GPPProblem fields (problem.py:50-71).
+ *   wtilde, i_eps : (ncouls, ngpown) complex, F-order  -> 2*ncouls*ngpown doubles
+ *   aqsntemp      : (ncouls, nbands) complex, F-order  (whole array; only the
+ *                   shard's columns are copied)
+ *   aqsmtemp      : (ngpown, nbands) complex, F-order  (whole array)
+ *   wx            : nw doubles (wx_band_indexed == 0, the reference's (NW,)
+ *                   vector, problem.py:70), or an (nw, nbands) F-order array
+ *                   (wx_band_indexed != 0, BerkeleyGW's wx_array(iw, n1)).
+ * The device always stores wx band-indexed, so the kernel evaluates every
+ * (band, igp, ig, iw) instance (no band-invariance shortcut).
+ * nw may be any value >= 1; the library processes it in groups of <= 4. */
+int gpp_upload(gpp_ctx* ctx, int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw,
+               const double* wtilde, const double* i_eps, const double* aqsntemp,
+               const double* aqsmtemp, const double* wx, int32_t wx_band_indexed,
+               int64_t band0, int64_t band1);
+
+/* Evaluate the uploaded problem.  Replaces evaluate_variant (kernel.py:98-114)
+ * and, through near_far, branch_stats (kernel.py:130-137).
+ *   achtemp, asxtemp : 2*nw doubles each (complex, interleaved)
+ *   near_far         : nullable; receives [near, far] instance counts over
+ *                      the evaluated (band, igp, ig, iw) instances
+ *   kernel_ms        : nullable; device time of the compute kernels (CUDA
+ *                      events), excluding the collective and the D2H copy
+ * With a communicator attached (gpp_comm_init) the per-rank partial sums and
+ * counts are combined with ncclAllReduce before they are returned. */
+int gpp_run(gpp_ctx* ctx, int32_t variant, double* achtemp, double* asxtemp,
+            int64_t* near_far, float* kernel_ms);
+
+/* Device-resident timing: `iters` back-to-back evaluations on the context's
+ * stream (compute kernels + finalize + allreduce when attached, no host
+ * copies).  total_ms = event time of the whole run; main_ms = summed event
+ * time of the main reduction kernel launches alone. */
+int gpp_time(gpp_ctx* ctx, int32_t variant, int32_t iters, float* total_ms, float* main_ms);
+
+/* Launch shape of the main kernel for the uploaded problem. */
+int gpp_kernel_info(gpp_ctx* ctx, int32_t variant, int32_t* registers_per_thread,
+                    int32_t* threads_per_block, int32_t* blocks_per_sm, int32_t* grid,
+                    int32_t* igp_tile, int32_t* band_chunk);
+
+/* NCCL plumbing for band sharding across ranks (one process per GPU).
+ * The unique id (128 bytes) is created on rank 0 and broadcast by the host
+ * (torch.distributed in the Python driver). */
+int gpp_comm_unique_id(unsigned char* id128);
+int gpp_comm_init(gpp_ctx* ctx, int nranks, int rank, const unsigned char* id128);
+
+/* Page-lock an existing host buffer so uploads from it run at DMA speed. */
+int gpp_host_register(void* ptr, size_t bytes);
+int gpp_host_unregister(void* ptr);
+
+/* FP64 (DFMA) pipe microbenchmark: independent FMA chains on every SM.
+ * Returns the achieved FP64 TFLOP/s (2 flops per DFMA) and the device time. */
+int gpp_fp64_peak(int device, int32_t iters, double* tflops, float* ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GPP_B200_H */

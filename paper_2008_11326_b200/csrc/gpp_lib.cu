@@ -1,0 +1,582 @@
+// gpp_lib.cu -- host side of libgpp_b200.so: the C ABI declared in
+// include/gpp_b200.h, the device-buffer manager, launch planning, the NCCL
+// band-shard combine and the FP64 peak microbenchmark.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gpp_b200.h"
+#include "gpp_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  const int code = (e == cudaErrorMemoryAllocation) ? GPP_ERR_OOM : GPP_ERR_CUDA;
+  return fail(code, std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                        cudaGetErrorString(e) + ")");
+}
+
+#define GPP_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);  \
+  } while (0)
+
+#define GPP_NCCL(call)                                                              \
+  do {                                                                              \
+    ncclResult_t _r = (call);                                                       \
+    if (_r != ncclSuccess)                                                          \
+      return fail(GPP_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(_r)); \
+  } while (0)
+
+// Restores the caller's current device on scope exit, so the library never
+// leaves torch (or any other caller) on a different device.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    err = cudaGetDevice(&prev);
+    if (err != cudaSuccess) return;
+    if (prev != dev) err = cudaSetDevice(dev);
+    ok = (err == cudaSuccess);
+  }
+  ~DeviceGuard() {
+    if (ok && prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <class T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t cap = 0;  // elements
+  cudaError_t ensure(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(n, 1) * sizeof(T));
+    if (e == cudaSuccess) cap = n;
+    return e;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct gpp_ctx {
+  int device = -1;
+  bool initialized = false;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int num_sms = 0;
+
+  // Problem (local band shard).
+  bool have_problem = false;
+  int64_t nbands = 0, ngpown = 0, ncouls = 0;
+  int nw = 0;
+
+  DevBuf<double2> wtilde, eps, aqsn, aqsm;
+  DevBuf<double> wxb;
+  DevBuf<double> partials;
+  DevBuf<unsigned long long> cpartials;
+  DevBuf<double> out;                  // 4 * nw
+  DevBuf<unsigned long long> counts;   // 2
+  double* h_out = nullptr;             // pinned staging
+  unsigned long long* h_counts = nullptr;
+  size_t h_out_cap = 0;
+  double* h_wx = nullptr;              // pinned staging for the expanded wx
+  size_t h_wx_cap = 0;
+
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+};
+
+namespace {
+
+int ensure_init(gpp_ctx* c) {
+  if (c->initialized) return GPP_OK;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (c->device >= n)
+    return fail(GPP_ERR_ARG, "device " + std::to_string(c->device) + " out of range (" +
+                                 std::to_string(n) + " devices)");
+  DeviceGuard g(c->device);
+  if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+  GPP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  for (auto& ev : c->ev) GPP_CUDA(cudaEventCreate(&ev));
+  GPP_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+  c->initialized = true;
+  return GPP_OK;
+}
+
+// ----- launch planning ------------------------------------------------------
+struct Plan {
+  int igp_t = 4;
+  int bchunk = gpp::kMaxChunk;
+  int n_igblk = 1, n_igptile = 1;
+  long long n_items = 1;
+  int grid = 1;
+  int blocks_per_sm = 1;
+  int regs = 0;
+};
+
+using KernelFn = void (*)(gpp::Params);
+
+template <int NW>
+KernelFn pick_fast(int igp_t) {
+  if (NW >= 4 || igp_t == 3) return gpp::gpp_main_kernel<gpp::FastPolicy, NW, 3>;
+  return gpp::gpp_main_kernel<gpp::FastPolicy, NW, (NW >= 4 ? 3 : 4)>;
+}
+
+template <class P>
+KernelFn pick_plain(int nw) {
+  switch (nw) {
+    case 1: return gpp::gpp_main_kernel<P, 1, 2>;
+    case 2: return gpp::gpp_main_kernel<P, 2, 2>;
+    case 3: return gpp::gpp_main_kernel<P, 3, 2>;
+    default: return gpp::gpp_main_kernel<P, 4, 2>;
+  }
+}
+
+KernelFn pick_kernel(int variant, int nw, int igp_t) {
+  switch (variant) {
+    case GPP_VARIANT_DIV: return pick_plain<gpp::PlainPolicy<0>>(nw);
+    case GPP_VARIANT_RCP: return pick_plain<gpp::PlainPolicy<1>>(nw);
+    default:
+      switch (nw) {
+        case 1: return pick_fast<1>(igp_t);
+        case 2: return pick_fast<2>(igp_t);
+        case 3: return pick_fast<3>(igp_t);
+        default: return pick_fast<4>(igp_t);
+      }
+  }
+}
+
+using FinalizeFn = void (*)(const double*, const unsigned long long*, int, int, int, int, int,
+                            double*, unsigned long long*);
+FinalizeFn pick_finalize(int nw) {
+  switch (nw) {
+    case 1: return gpp::gpp_finalize_kernel<1>;
+    case 2: return gpp::gpp_finalize_kernel<2>;
+    case 3: return gpp::gpp_finalize_kernel<3>;
+    default: return gpp::gpp_finalize_kernel<4>;
+  }
+}
+
+// igp tile for the fast kernel: the size in {4, 3} wasting the fewest padded
+// igp columns, ties to 4.
+int choose_igp_tile(int64_t ngpown) {
+  int best = 4;
+  int64_t best_waste = (ngpown + 3) / 4 * 4 - ngpown;
+  const int64_t w3 = (ngpown + 2) / 3 * 3 - ngpown;
+  if (w3 < best_waste) best = 3;
+  return best;
+}
+
+int make_plan(gpp_ctx* c, int variant, int nw_group, Plan* pl) {
+  // The plain (as-written) variants keep two igp per thread and the fast
+  // kernel drops to 3 at four frequencies: both choices avoid spills under
+  // the 128-register budget of __launch_bounds__(256, 2).
+  if (variant != GPP_VARIANT_RCP_SQ)
+    pl->igp_t = 2;
+  else
+    pl->igp_t = nw_group >= 4 ? 3 : choose_igp_tile(c->ngpown);
+  pl->n_igblk = static_cast<int>((c->ncouls + gpp::kThreads - 1) / gpp::kThreads);
+  pl->n_igptile = static_cast<int>((c->ngpown + pl->igp_t - 1) / pl->igp_t);
+  KernelFn fn = pick_kernel(variant, nw_group, pl->igp_t);
+  int bps = 0;
+  GPP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, gpp::kThreads, 0));
+  cudaFuncAttributes attr;
+  GPP_CUDA(cudaFuncGetAttributes(&attr, fn));
+  pl->regs = attr.numRegs;
+  pl->blocks_per_sm = std::max(bps, 1);
+  const long long slots = static_cast<long long>(pl->blocks_per_sm) * c->num_sms;
+  // Band chunk: as long as possible (amortises the per-item state load) while
+  // leaving >= 32 items per resident CTA so the static round-robin balances.
+  int bchunk = static_cast<int>(std::min<int64_t>(gpp::kMaxChunk, c->nbands));
+  auto items_for = [&](int bc) {
+    return static_cast<long long>(pl->n_igblk) * pl->n_igptile * ((c->nbands + bc - 1) / bc);
+  };
+  while (bchunk > 8 && items_for(bchunk) < 32 * slots) bchunk = (bchunk + 1) / 2;
+  pl->bchunk = bchunk;
+  pl->n_items = items_for(bchunk);
+  pl->grid = static_cast<int>(std::min<long long>(slots, pl->n_items));
+  return GPP_OK;
+}
+
+int nw_groups(int nw, std::vector<std::pair<int, int>>* groups) {
+  groups->clear();
+  for (int iw0 = 0; iw0 < nw; iw0 += gpp::kMaxNwGroup)
+    groups->emplace_back(iw0, std::min(gpp::kMaxNwGroup, nw - iw0));
+  return GPP_OK;
+}
+
+// Enqueue one full evaluation on c->stream.  If ev_main is non-null, the
+// main kernels of all frequency groups are bracketed by ev_main[0..1].
+int enqueue_eval(gpp_ctx* c, int variant, cudaEvent_t* ev_main, bool allreduce) {
+  std::vector<std::pair<int, int>> groups;
+  nw_groups(c->nw, &groups);
+  bool first = true;
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    const int iw0 = groups[gi].first, nwg = groups[gi].second;
+    Plan pl;
+    int rc = make_plan(c, variant, nwg, &pl);
+    if (rc) return rc;
+    GPP_CUDA(c->partials.ensure(static_cast<size_t>(pl.grid) * 4 * gpp::kMaxNwGroup));
+    GPP_CUDA(c->cpartials.ensure(static_cast<size_t>(pl.grid) * 2));
+    gpp::Params p;
+    p.wtilde = c->wtilde.ptr;
+    p.eps = c->eps.ptr;
+    p.aqsn = c->aqsn.ptr;
+    p.aqsm = c->aqsm.ptr;
+    p.wxb = c->wxb.ptr;
+    p.ncouls = static_cast<int>(c->ncouls);
+    p.ngpown = static_cast<int>(c->ngpown);
+    p.nbands = static_cast<int>(c->nbands);
+    p.nw_total = c->nw;
+    p.iw0 = iw0;
+    p.n_igblk = pl.n_igblk;
+    p.n_igptile = pl.n_igptile;
+    p.bchunk = pl.bchunk;
+    p.n_items = pl.n_items;
+    p.partials = c->partials.ptr;
+    p.cpartials = c->cpartials.ptr;
+    KernelFn fn = pick_kernel(variant, nwg, pl.igp_t);
+    if (ev_main && gi == 0) GPP_CUDA(cudaEventRecord(ev_main[0], c->stream));
+    fn<<<pl.grid, gpp::kThreads, 0, c->stream>>>(p);
+    GPP_CUDA(cudaGetLastError());
+    if (ev_main && gi + 1 == groups.size()) GPP_CUDA(cudaEventRecord(ev_main[1], c->stream));
+    pick_finalize(nwg)<<<1, 256, 0, c->stream>>>(c->partials.ptr, c->cpartials.ptr, pl.grid,
+                                                  c->nw, iw0, variant == GPP_VARIANT_RCP_SQ,
+                                                  first ? 1 : 0, c->out.ptr, c->counts.ptr);
+    GPP_CUDA(cudaGetLastError());
+    first = false;
+  }
+  if (allreduce && c->comm && c->nranks > 1) {
+    GPP_NCCL(ncclGroupStart());
+    GPP_NCCL(ncclAllReduce(c->out.ptr, c->out.ptr, 4 * c->nw, ncclDouble, ncclSum, c->comm,
+                           c->stream));
+    GPP_NCCL(ncclAllReduce(c->counts.ptr, c->counts.ptr, 2, ncclUint64, ncclSum, c->comm,
+                           c->stream));
+    GPP_NCCL(ncclGroupEnd());
+  }
+  return GPP_OK;
+}
+
+int check_variant(int32_t variant) {
+  if (variant < GPP_VARIANT_DIV || variant > GPP_VARIANT_RCP_SQ)
+    return fail(GPP_ERR_ARG, "unknown variant " + std::to_string(variant) +
+                                 " (expected 0=div, 1=rcp, 2=rcp_sq)");
+  return GPP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gpp_abi_version(void) { return GPP_ABI_VERSION; }
+
+const char* gpp_last_error(void) { return g_last_error.c_str(); }
+
+int gpp_device_count(int* count) {
+  if (!count) return fail(GPP_ERR_ARG, "count is NULL");
+  *count = 0;
+  GPP_CUDA(cudaGetDeviceCount(count));
+  return GPP_OK;
+}
+
+int gpp_create(gpp_ctx** ctx, int device) {
+  if (!ctx) return fail(GPP_ERR_ARG, "ctx is NULL");
+  *ctx = nullptr;
+  if (device < 0) return fail(GPP_ERR_ARG, "device must be >= 0");
+  gpp_ctx* c = new (std::nothrow) gpp_ctx();
+  if (!c) return fail(GPP_ERR_OOM, "host allocation failed");
+  c->device = device;
+  *ctx = c;
+  return GPP_OK;
+}
+
+void gpp_destroy(gpp_ctx* c) {
+  if (!c) return;
+  if (c->initialized) {
+    DeviceGuard g(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm) ncclCommDestroy(c->comm);
+    c->wtilde.release();
+    c->eps.release();
+    c->aqsn.release();
+    c->aqsm.release();
+    c->wxb.release();
+    c->partials.release();
+    c->cpartials.release();
+    c->out.release();
+    c->counts.release();
+    if (c->h_out) cudaFreeHost(c->h_out);
+    if (c->h_counts) cudaFreeHost(c->h_counts);
+    if (c->h_wx) cudaFreeHost(c->h_wx);
+    for (auto& ev : c->ev)
+      if (ev) cudaEventDestroy(ev);
+    if (c->stream) cudaStreamDestroy(c->stream);
+  }
+  delete c;
+}
+
+int gpp_upload(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw,
+               const double* wtilde, const double* i_eps, const double* aqsntemp,
+               const double* aqsmtemp, const double* wx, int32_t wx_band_indexed,
+               int64_t band0, int64_t band1) {
+  if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
+  if (nbands < 1 || ngpown < 1 || ncouls < 1)
+    return fail(GPP_ERR_ARG, "nbands, ngpown and ncouls must all be at least 1");
+  if (nw < 1) return fail(GPP_ERR_ARG, "nw must be at least 1");
+  if (!wtilde || !i_eps || !aqsntemp || !aqsmtemp || !wx)
+    return fail(GPP_ERR_ARG, "input array pointer is NULL");
+  if (band0 < 0 || band1 > nbands || band0 >= band1)
+    return fail(GPP_ERR_ARG, "band range [" + std::to_string(band0) + ", " +
+                                 std::to_string(band1) + ") is empty or outside [0, " +
+                                 std::to_string(nbands) + ")");
+  const int64_t kIntMax = 0x7fffffff;
+  if (ncouls > kIntMax || ngpown > kIntMax || nbands > kIntMax ||
+      (ncouls + gpp::kThreads) * (ngpown + gpp::kMaxIgpTile) > (int64_t{1} << 40))
+    return fail(GPP_ERR_ARG, "problem dimensions exceed the supported range");
+  int rc = ensure_init(c);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
+  if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+
+  const int64_t nb = band1 - band0;
+  const size_t n_wt = static_cast<size_t>(ncouls) * ngpown;
+  const size_t n_an = static_cast<size_t>(ncouls) * nb;
+  const size_t n_am = static_cast<size_t>(ngpown) * nb;
+  const size_t n_wx = static_cast<size_t>(nb) * nw;
+  GPP_CUDA(c->wtilde.ensure(n_wt));
+  GPP_CUDA(c->eps.ensure(n_wt));
+  GPP_CUDA(c->aqsn.ensure(n_an));
+  GPP_CUDA(c->aqsm.ensure(n_am));
+  GPP_CUDA(c->wxb.ensure(n_wx));
+  GPP_CUDA(c->out.ensure(4 * static_cast<size_t>(nw)));
+  GPP_CUDA(c->counts.ensure(2));
+  if (c->h_out_cap < 4 * static_cast<size_t>(nw)) {
+    if (c->h_out) cudaFreeHost(c->h_out);
+    c->h_out = nullptr;
+    c->h_out_cap = 0;
+    GPP_CUDA(cudaMallocHost(&c->h_out, 4 * sizeof(double) * nw));
+    c->h_out_cap = 4 * static_cast<size_t>(nw);
+  }
+  if (!c->h_counts) GPP_CUDA(cudaMallocHost(&c->h_counts, 2 * sizeof(unsigned long long)));
+  if (c->h_wx_cap < n_wx) {
+    if (c->h_wx) cudaFreeHost(c->h_wx);
+    c->h_wx = nullptr;
+    c->h_wx_cap = 0;
+    GPP_CUDA(cudaMallocHost(&c->h_wx, n_wx * sizeof(double)));
+    c->h_wx_cap = n_wx;
+  }
+  // wx -> band-indexed [band][iw] for the shard.
+  if (wx_band_indexed) {
+    std::memcpy(c->h_wx, wx + static_cast<size_t>(band0) * nw, n_wx * sizeof(double));
+  } else {
+    for (int64_t b = 0; b < nb; ++b)
+      std::memcpy(c->h_wx + static_cast<size_t>(b) * nw, wx, nw * sizeof(double));
+  }
+  cudaStream_t s = c->stream;
+  GPP_CUDA(cudaMemcpyAsync(c->wtilde.ptr, wtilde, n_wt * sizeof(double2), cudaMemcpyHostToDevice, s));
+  GPP_CUDA(cudaMemcpyAsync(c->eps.ptr, i_eps, n_wt * sizeof(double2), cudaMemcpyHostToDevice, s));
+  GPP_CUDA(cudaMemcpyAsync(c->aqsn.ptr, aqsntemp + 2 * static_cast<size_t>(band0) * ncouls,
+                           n_an * sizeof(double2), cudaMemcpyHostToDevice, s));
+  GPP_CUDA(cudaMemcpyAsync(c->aqsm.ptr, aqsmtemp + 2 * static_cast<size_t>(band0) * ngpown,
+                           n_am * sizeof(double2), cudaMemcpyHostToDevice, s));
+  GPP_CUDA(cudaMemcpyAsync(c->wxb.ptr, c->h_wx, n_wx * sizeof(double), cudaMemcpyHostToDevice, s));
+  GPP_CUDA(cudaStreamSynchronize(s));
+  c->nbands = nb;
+  c->ngpown = ngpown;
+  c->ncouls = ncouls;
+  c->nw = nw;
+  c->have_problem = true;
+  return GPP_OK;
+}
+
+int gpp_run(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp, int64_t* near_far,
+            float* kernel_ms) {
+  if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
+  int rc = check_variant(variant);
+  if (rc) return rc;
+  if (!achtemp || !asxtemp) return fail(GPP_ERR_ARG, "output pointer is NULL");
+  if (!c->have_problem) return fail(GPP_ERR_ARG, "no problem uploaded");
+  DeviceGuard g(c->device);
+  if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+  GPP_CUDA(cudaEventRecord(c->ev[2], c->stream));
+  rc = enqueue_eval(c, variant, nullptr, false);
+  if (rc) return rc;
+  GPP_CUDA(cudaEventRecord(c->ev[3], c->stream));
+  if (c->comm && c->nranks > 1) {
+    GPP_NCCL(ncclGroupStart());
+    GPP_NCCL(ncclAllReduce(c->out.ptr, c->out.ptr, 4 * c->nw, ncclDouble, ncclSum, c->comm,
+                           c->stream));
+    GPP_NCCL(ncclAllReduce(c->counts.ptr, c->counts.ptr, 2, ncclUint64, ncclSum, c->comm,
+                           c->stream));
+    GPP_NCCL(ncclGroupEnd());
+  }
+  GPP_CUDA(cudaMemcpyAsync(c->h_out, c->out.ptr, 4 * sizeof(double) * c->nw,
+                           cudaMemcpyDeviceToHost, c->stream));
+  GPP_CUDA(cudaMemcpyAsync(c->h_counts, c->counts.ptr, 2 * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, c->stream));
+  GPP_CUDA(cudaStreamSynchronize(c->stream));
+  std::memcpy(achtemp, c->h_out, 2 * sizeof(double) * c->nw);
+  std::memcpy(asxtemp, c->h_out + 2 * c->nw, 2 * sizeof(double) * c->nw);
+  if (near_far) {
+    near_far[0] = static_cast<int64_t>(c->h_counts[0]);
+    near_far[1] = static_cast<int64_t>(c->h_counts[1]);
+  }
+  if (kernel_ms) GPP_CUDA(cudaEventElapsedTime(kernel_ms, c->ev[2], c->ev[3]));
+  return GPP_OK;
+}
+
+int gpp_time(gpp_ctx* c, int32_t variant, int32_t iters, float* total_ms, float* main_ms) {
+  if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
+  int rc = check_variant(variant);
+  if (rc) return rc;
+  if (iters < 1) return fail(GPP_ERR_ARG, "iters must be at least 1");
+  if (!c->have_problem) return fail(GPP_ERR_ARG, "no problem uploaded");
+  DeviceGuard g(c->device);
+  if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+  std::vector<cudaEvent_t> evs(2 * static_cast<size_t>(iters));
+  for (auto& e : evs) GPP_CUDA(cudaEventCreate(&e));
+  int result = GPP_OK;
+  do {
+    cudaError_t e = cudaEventRecord(c->ev[2], c->stream);
+    if (e != cudaSuccess) { result = cuda_fail(e, "cudaEventRecord"); break; }
+    for (int i = 0; i < iters && result == GPP_OK; ++i)
+      result = enqueue_eval(c, variant, &evs[2 * static_cast<size_t>(i)], true);
+    if (result) break;
+    e = cudaEventRecord(c->ev[3], c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) { result = cuda_fail(e, "gpp_time sync"); break; }
+    float tot = 0.f, mm = 0.f;
+    cudaEventElapsedTime(&tot, c->ev[2], c->ev[3]);
+    for (int i = 0; i < iters; ++i) {
+      float x = 0.f;
+      cudaEventElapsedTime(&x, evs[2 * i], evs[2 * i + 1]);
+      mm += x;
+    }
+    if (total_ms) *total_ms = tot;
+    if (main_ms) *main_ms = mm;
+  } while (0);
+  for (auto& e : evs) cudaEventDestroy(e);
+  return result;
+}
+
+int gpp_kernel_info(gpp_ctx* c, int32_t variant, int32_t* registers_per_thread,
+                    int32_t* threads_per_block, int32_t* blocks_per_sm, int32_t* grid,
+                    int32_t* igp_tile, int32_t* band_chunk) {
+  if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
+  int rc = check_variant(variant);
+  if (rc) return rc;
+  if (!c->have_problem) return fail(GPP_ERR_ARG, "no problem uploaded");
+  DeviceGuard g(c->device);
+  if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+  Plan pl;
+  rc = make_plan(c, variant, std::min(c->nw, gpp::kMaxNwGroup), &pl);
+  if (rc) return rc;
+  if (registers_per_thread) *registers_per_thread = pl.regs;
+  if (threads_per_block) *threads_per_block = gpp::kThreads;
+  if (blocks_per_sm) *blocks_per_sm = pl.blocks_per_sm;
+  if (grid) *grid = pl.grid;
+  if (igp_tile) *igp_tile = pl.igp_t;
+  if (band_chunk) *band_chunk = pl.bchunk;
+  return GPP_OK;
+}
+
+int gpp_comm_unique_id(unsigned char* id128) {
+  if (!id128) return fail(GPP_ERR_ARG, "id buffer is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+  ncclUniqueId id;
+  GPP_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(id128, &id, sizeof(id));
+  return GPP_OK;
+}
+
+int gpp_comm_init(gpp_ctx* c, int nranks, int rank, const unsigned char* id128) {
+  if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
+  if (!id128) return fail(GPP_ERR_ARG, "id buffer is NULL");
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(GPP_ERR_ARG, "rank " + std::to_string(rank) + " outside [0, " +
+                                 std::to_string(nranks) + ")");
+  int rc = ensure_init(c);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
+  if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+  if (c->comm) {
+    ncclCommDestroy(c->comm);
+    c->comm = nullptr;
+  }
+  c->nranks = nranks;
+  c->rank = rank;
+  if (nranks == 1) return GPP_OK;
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  GPP_NCCL(ncclCommInitRank(&c->comm, nranks, id, rank));
+  return GPP_OK;
+}
+
+int gpp_host_register(void* ptr, size_t bytes) {
+  if (!ptr || bytes == 0) return fail(GPP_ERR_ARG, "empty host range");
+  GPP_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
+  return GPP_OK;
+}
+
+int gpp_host_unregister(void* ptr) {
+  if (!ptr) return fail(GPP_ERR_ARG, "ptr is NULL");
+  GPP_CUDA(cudaHostUnregister(ptr));
+  return GPP_OK;
+}
+
+int gpp_fp64_peak(int device, int32_t iters, double* tflops, float* ms) {
+  if (device < 0 || iters < 1) return fail(GPP_ERR_ARG, "bad device or iters");
+  int n = 0;
+  GPP_CUDA(cudaGetDeviceCount(&n));
+  if (device >= n) return fail(GPP_ERR_ARG, "device out of range");
+  DeviceGuard g(device);
+  if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+  int sms = 0;
+  GPP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  double* sink = nullptr;
+  GPP_CUDA(cudaMalloc(&sink, 256 * sizeof(double)));
+  cudaEvent_t a, b;
+  GPP_CUDA(cudaEventCreate(&a));
+  GPP_CUDA(cudaEventCreate(&b));
+  const int grid = sms * 8;  // 8 x 256 threads = 64 warps per SM
+  gpp::fp64_peak_kernel<<<grid, 256>>>(sink, std::max(1, iters / 10), 0.999999, 1e-7);  // warm
+  GPP_CUDA(cudaEventRecord(a));
+  gpp::fp64_peak_kernel<<<grid, 256>>>(sink, iters, 0.999999, 1e-7);
+  GPP_CUDA(cudaEventRecord(b));
+  GPP_CUDA(cudaEventSynchronize(b));
+  float t = 0.f;
+  GPP_CUDA(cudaEventElapsedTime(&t, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  const double flops = 2.0 * 8.0 * static_cast<double>(iters) * grid * 256.0;
+  if (tflops) *tflops = flops / (t * 1e-3) / 1e12;
+  if (ms) *ms = t;
+  return GPP_OK;
+}
+
+}  // extern "C"

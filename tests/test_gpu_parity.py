@@ -1,0 +1,176 @@
+"""Parity of the sm_100a kernels (through the C ABI) with the reference.
+
+Gate (BASELINE.json north_star): max_rel_error <= 1e-10 against the
+reference's achtemp/asxtemp on identical synthetic inputs, and near/far
+counts EXACTLY equal to the reference's branch_stats (integer work).
+Small cases compare against golden fixtures generated from the unmodified
+reference (tests/golden/make_golden.py) and against the oracle run here;
+paper / sweep / weak sizes against the committed reference outputs.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import as_complex, load_cases
+from oracle import gpp_oracle as orc
+from paper_2008_11326_b200 import (
+    GPPContext,
+    GPPProblem,
+    branch_stats,
+    evaluate,
+    evaluate_variant,
+    reference_result,
+    run_version,
+    synth_problem,
+)
+from paper_2008_11326_b200.problem import max_rel_error
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10  # north_star: results within 1e-10 relative error
+SMALL = load_cases("gpp_small.json")
+BIG = load_cases("gpp_big.json")
+
+
+class _R:
+    def __init__(self, d):
+        self.achtemp = as_complex(d["achtemp"])
+        self.asxtemp = as_complex(d["asxtemp"])
+
+
+def _ids(cases):
+    return [f"{tuple(c['dims'])}-s{c['seed']}-nw{c['nw']}" for c in cases]
+
+
+@pytest.mark.parametrize("case", SMALL, ids=_ids(SMALL))
+@pytest.mark.parametrize("variant", ["div", "rcp", "rcp_sq"])
+def test_small_cases_vs_reference(case, variant):
+    p = synth_problem(*case["dims"], seed=case["seed"], nw=case["nw"])
+    got, stats, _ = evaluate(p, variant)
+    assert max_rel_error(got, _R(case["reference_result"])) <= TOL
+    assert max_rel_error(got, _R(case["evaluate_variant"][variant])) <= TOL
+    assert [stats.instances, stats.near, stats.far] == case["branch_stats"][variant]
+
+
+@pytest.mark.parametrize("case", BIG, ids=_ids(BIG))
+def test_big_cases_vs_reference(case):
+    nb, ng, nc = case["dims"]
+    p = synth_problem(nb, ng, nc, seed=case["seed"], nw=case["nw"], check=nb * ng * nc < 10**10)
+    got, stats, _ = evaluate(p, "rcp_sq")
+    want = _R(case.get("reference_result") or case["evaluate_variant"]["rcp_sq"])
+    err = max_rel_error(got, want)
+    assert err <= TOL, err
+    assert [stats.instances, stats.near, stats.far] == case["branch_stats"]["rcp_sq"]
+
+
+def test_plain_variants_paper_size():
+    case = next(c for c in BIG if c["dims"] == [512, 66, 32768] and c["seed"] == 1 and c["nw"] == 2)
+    p = synth_problem(512, 66, 32768, seed=1)
+    want = _R(case["reference_result"])
+    for variant in ("div", "rcp"):
+        got, stats, _ = evaluate(p, variant)
+        assert max_rel_error(got, want) <= TOL, variant
+        assert stats.far == case["branch_stats"]["rcp_sq"][2]
+
+
+def test_kat_golden_64x64x512():
+    from paper_2008_11326_b200.problem import load_golden
+    from conftest import GOLDEN
+
+    dims, seed, golden = load_golden(GOLDEN / "gpp-golden-seed42-64x64x512.json")
+    p = synth_problem(*dims, seed=seed)
+    assert max_rel_error(reference_result(p), golden) <= 1e-12
+    assert max_rel_error(evaluate_variant(p, "rcp_sq"), golden) <= 1e-12
+
+
+@pytest.mark.parametrize("nw", [1, 4, 5, 9])
+def test_other_frequency_counts_vs_oracle(nw):
+    """nw is a parameter (groups of <= 4 per launch); oracle on the same input."""
+    p = synth_problem(24, 7, 300, seed=11, nw=nw)
+    want = orc.reference_result(p)
+    inst, near, far = orc.branch_stats(p, "rcp_sq")
+    for variant in ("rcp_sq", "div"):
+        got, stats, _ = evaluate(p, variant)
+        assert max_rel_error(got, want) <= TOL
+        assert (stats.instances, stats.near, stats.far) == (inst, near, far)
+
+
+def test_band_indexed_wx_vs_oracle():
+    """BerkeleyGW's wx_array(iw, n1): every band has its own frequencies."""
+    base = synth_problem(40, 9, 700, seed=3)
+    rng = np.random.default_rng(5)
+    wxb = np.asfortranarray(rng.uniform(1.0, 2.0, size=(3, 40)))
+    p = GPPProblem(40, 9, 700, base.wtilde, base.i_eps, base.aqsntemp, base.aqsmtemp, wxb)
+    want = orc.reference_result(p)
+    inst, near, far = orc.branch_stats(p, "rcp_sq")
+    for variant in ("rcp_sq", "rcp", "div"):
+        got, stats, _ = evaluate(p, variant)
+        assert max_rel_error(got, want) <= TOL, variant
+        assert (stats.instances, stats.near, stats.far) == (inst, near, far), variant
+
+
+def test_band_shards_sum_to_whole():
+    """Band sharding (the multi-GPU partition) on one device: shards add up."""
+    p = synth_problem(64, 33, 1000, seed=1, nw=3)
+    whole, (n0, f0), _ = _run(p, None)
+    parts = [_run(p, r) for r in ((0, 17), (17, 40), (40, 64))]
+    ach = sum(r[0].achtemp for r in parts)
+    asx = sum(r[0].asxtemp for r in parts)
+    assert max_rel_error(type(whole)(achtemp=ach, asxtemp=asx), whole) <= 1e-12
+    assert sum(r[1][0] for r in parts) == n0 and sum(r[1][1] for r in parts) == f0
+
+
+def _run(p, band_range):
+    ctx = GPPContext(0)
+    try:
+        ctx.upload(p, band_range)
+        return ctx.run("rcp_sq")
+    finally:
+        ctx.close()
+
+
+def test_deterministic_bitwise():
+    p = synth_problem(128, 66, 4096, seed=1, nw=3)
+    a = evaluate_variant(p, "rcp_sq")
+    b = evaluate_variant(p, "rcp_sq")
+    assert np.array_equal(a.achtemp, b.achtemp) and np.array_equal(a.asxtemp, b.asxtemp)
+
+
+def test_writeable_inputs_are_reuploaded():
+    p = synth_problem(8, 8, 64, seed=1)
+    arrs = {k: np.array(getattr(p, k), order="F") for k in ("wtilde", "i_eps", "aqsntemp", "aqsmtemp", "wx")}
+    q = GPPProblem(8, 8, 64, **arrs)
+    first = evaluate_variant(q, "rcp_sq")
+    arrs["aqsntemp"] *= 2.0
+    second = evaluate_variant(q, "rcp_sq")
+    np.testing.assert_allclose(second.achtemp, 2.0 * first.achtemp, rtol=1e-12)
+
+
+def test_run_version_counters_match_reference():
+    case = next(c for c in SMALL if c["dims"] == [64, 64, 512] and c["seed"] == 7 and c["nw"] == 2)
+    p = synth_problem(64, 64, 512, seed=7)
+    for name, want in case["counters"].items():
+        art = run_version(p, name)
+        assert art.counters.to_dict() == want, name
+        assert max_rel_error(art.result, _R(case["reference_result"])) <= TOL
+        assert art.registers_per_thread > 0 and art.kernel_s > 0
+
+
+def test_branch_stats_api():
+    p = synth_problem(4, 4, 64, seed=7)
+    s = branch_stats(p, "div")
+    assert s.near > 0 and s.far > 0 and s.instances == 2 * 4 * 4 * 64
+
+
+def test_degenerate_inputs():
+    """wtilde == 0 makes delw vanish: near iff |wdiff| > 0.5, never far."""
+    p = synth_problem(5, 3, 40, seed=1)
+    wt = np.array(p.wtilde, order="F")
+    wt[:7, 1] = 0.0
+    q = GPPProblem(5, 3, 40, wt, p.i_eps, p.aqsntemp, p.aqsmtemp, p.wx)
+    want = orc.reference_result(q)
+    inst, near, far = orc.branch_stats(q, "div")
+    for variant in ("rcp_sq", "div", "rcp"):
+        got, stats, _ = evaluate(q, variant)
+        assert max_rel_error(got, want) <= TOL, variant
+        assert (stats.near, stats.far) == (near, far), variant
