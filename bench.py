@@ -1,0 +1,447 @@
+#!/usr/bin/env python
+"""GPP self-energy bench on B200: one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Workload (BASELINE.json configs[1]): the paper size (nbands, ngpown, ncouls) =
+(512, 66, 32768) with 3 frequencies, synth_problem seed 1 (3.5 % far-branch
+instances; seed 42 never takes the far branch).  At N GPUs the
+band (n1) loop is sharded across ranks (strong scaling, BASELINE configs[2]);
+the per-rank partial achtemp/asxtemp and branch counts are combined by one
+NCCL allreduce inside the library.
+
+A step = one full evaluation of the reduction (main kernel + deterministic
+finalize (+ allreduce)).  `value` = algorithmic FP64 FLOPs of the whole job
+(the reference's analytic count, rooflab/gpp/kernel.py:191-212 with the
+kernel's exact near/far counts) / device time (CUDA events, max over ranks).
+`e2e` = the same metric through the public API with pinned host inputs:
+H2D of every input, the evaluation and the D2H of the result each step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "GPP FP64 TFLOP/s (ncu-counted) per B200 & % of FP64 peak; 1/2/4/8-GPU time"
+WORKLOADS = {
+    "paper": (512, 66, 32768),
+    "tiny": (32, 8, 512),
+    "weak": (4096, 528, 65536),
+}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default="paper")
+    ap.add_argument("--nw", type=int, default=3)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--variant", choices=("rcp_sq", "rcp", "div"), default="rcp_sq")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------
+# distributed plumbing
+# ----------------------------------------------------------------------------
+class Dist:
+    def __init__(self, gpus: int):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        if self.world != gpus:
+            raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={self.world}; launch with torchrun for N>1")
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+
+            torch.cuda.set_device(self.local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local_rank))
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def sync(self):
+        import torch
+
+        torch.cuda.synchronize()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def bcast_bytes(self, payload: bytes | None) -> bytes:
+        if not self.pg:
+            return payload
+        obj = [payload]
+        self.pg.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+def band_range(nbands: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced band shard [b0, b1) of rank."""
+    base, extra = divmod(nbands, world)
+    b0 = rank * base + min(rank, extra)
+    return b0, b0 + base + (1 if rank < extra else 0)
+
+
+# ----------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ----------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, devices):
+        self.devices = devices
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", ",".join(str(d) for d in self.devices)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 8:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        pw = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i] == "Active"})
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(mx) if mx else None,
+            "power_w_max": max(pw) if pw else None,
+            "samples": len(self.rows),
+            "reasons": reasons,
+        }
+
+
+# ----------------------------------------------------------------------------
+# CPU baseline (reference CPU path, restated in oracle/): rank 0 only
+# ----------------------------------------------------------------------------
+def _cpu_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+
+        n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def _igp_slice(problem, g0: int, g1: int):
+    from paper_2008_11326_b200 import GPPProblem
+
+    return GPPProblem(problem.nbands, g1 - g0, problem.ncouls,
+                      np.asfortranarray(problem.wtilde[:, g0:g1]), np.asfortranarray(problem.i_eps[:, g0:g1]),
+                      problem.aqsntemp, np.asfortranarray(problem.aqsmtemp[g0:g1, :]), problem.wx)
+
+
+def cpu_reference_steps(problem, steps: int, warmup: int, igp_per_step: int):
+    """Time the reference's production CPU path (evaluate_variant, the ZGEMM-
+    factored numpy code, restated in oracle/gpp_oracle.py) on igp slices of
+    the workload: every step evaluates `igp_per_step` igp columns of the full
+    problem, rotating through all of them.  Returns (flops, seconds) of the
+    timed steps; FLOPs are the reference's analytic count of each slice."""
+    from oracle import gpp_oracle as orc
+    from paper_2008_11326_b200.counters import algorithmic_flops
+
+    ng = problem.ngpown
+    slices = [(g, min(g + igp_per_step, ng)) for g in range(0, ng, igp_per_step)]
+    subs = [_igp_slice(problem, a, b) for a, b in slices]
+    fl = []
+    for s in subs:
+        _, near, far = orc.branch_stats(s, "rcp_sq")
+        fl.append(algorithmic_flops(s.nbands, s.ngpown, s.ncouls, len(s.wx), near, far))
+    for i in range(warmup):
+        orc.evaluate_variant(subs[i % len(subs)], "rcp_sq")
+    flops = 0
+    secs = 0.0
+    for i in range(steps):
+        k = i % len(subs)
+        t0 = time.perf_counter()
+        orc.evaluate_variant(subs[k], "rcp_sq")
+        secs += time.perf_counter() - t0
+        flops += fl[k]
+    return flops, secs
+
+
+# ----------------------------------------------------------------------------
+def load_profile_summary():
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except json.JSONDecodeError:
+            return None
+    return None
+
+
+def golden_parity(result, workload, seed, nw):
+    g = ROOT / "tests" / "golden" / "gpp_big.json"
+    if not g.exists():
+        return None
+    dims = list(WORKLOADS[workload])
+    for c in json.loads(g.read_text())["cases"]:
+        if c["dims"] == dims and c["seed"] == seed and c["nw"] == nw:
+            from paper_2008_11326_b200.problem import GPPResult, max_rel_error
+
+            src = c.get("reference_result") or c["evaluate_variant"]["rcp_sq"]
+            want = GPPResult(np.array([complex(*z) for z in src["achtemp"]]),
+                             np.array([complex(*z) for z in src["asxtemp"]]))
+            return {"max_rel_err_vs_reference": max_rel_error(result, want),
+                    "branch_stats_reference": c["branch_stats"]["rcp_sq"]}
+    return None
+
+
+def run_reference(args, dist: Dist):
+    """--impl reference: the reference's CPU path on this host (rank 0 only)."""
+    if dist.rank != 0:
+        return
+    from paper_2008_11326_b200 import synth_problem
+
+    dims = WORKLOADS[args.workload]
+    p = synth_problem(*dims, seed=args.seed, nw=args.nw, check=False)
+    igp_per_step = 6
+    flops, secs = cpu_reference_steps(p, args.steps, args.warmup, igp_per_step)
+    value = flops / secs / 1e12
+    cores = _cpu_threads()
+    sample = (f"each step = reference evaluate_variant('rcp_sq') (ZGEMM-factored numpy, "
+              f"oracle/gpp_oracle.py) on {igp_per_step} of {dims[1]} igp columns of the full "
+              f"{dims} nw={args.nw} problem, rotating")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": f"synthetic (synth_problem seed {args.seed})",
+        "config": _config(args, dims),
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                         "sample": sample, "cpu_count": os.cpu_count()},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config(args, dims):
+    return {
+        "workload": f"{args.workload} (nbands, ngpown, ncouls) = {dims}, nw={args.nw}",
+        "nbands": dims[0], "ngpown": dims[1], "ncouls": dims[2], "nw": args.nw, "seed": args.seed,
+        "variant": args.variant,
+        "parallelism": f"band-shard x{args.gpus}" + (" + NCCL allreduce" if args.gpus > 1 else ""),
+        "l2": "inputs (footprint > 126 MB L2) stream from HBM each step; no flush",
+    }
+
+
+def run_ours(args, dist: Dist):
+    from paper_2008_11326_b200 import GPPContext, comm_unique_id, fp64_peak, synth_problem
+    from paper_2008_11326_b200._lib import load
+    from paper_2008_11326_b200.counters import algorithmic_flops
+
+    dims = WORKLOADS[args.workload]
+    nb, ng, nc = dims
+    device = dist.local_rank
+    p = synth_problem(nb, ng, nc, seed=args.seed, nw=args.nw, check=False)
+    b0, b1 = band_range(nb, dist.world, dist.rank)
+
+    load()
+    # FP64 roofline denominator: measured live on this device (MEASURED_PEAKS.json has no FP64).
+    fp64_peak(device, 20_000)
+    peak_tf, _ = fp64_peak(device, 300_000)
+
+    ctx = GPPContext(device)
+    if dist.world > 1:
+        uid = dist.bcast_bytes(comm_unique_id() if dist.rank == 0 else None)
+        ctx.comm_init(dist.world, dist.rank, uid)
+    ctx.upload(p, (b0, b1))
+    result, (near, far), _ = ctx.run(args.variant)  # combined over ranks
+    info = ctx.kernel_info(args.variant)
+    flops_job = algorithmic_flops(nb, ng, nc, args.nw, near, far)
+    n_groups = -(-args.nw // 4)
+    launches_per_step = 2 * n_groups
+
+    # ---- device-resident timed region -----------------------------------
+    ctx.time(args.variant, args.warmup)
+    dist.barrier()
+    dist.sync()
+    clocks = Clocks(list(range(dist.world)) if dist.rank == 0 else [])
+    if dist.rank == 0:
+        clocks.start()
+    total_ms, main_ms = ctx.time(args.variant, args.steps)
+    dist.sync()
+    dist.barrier()
+    clk = clocks.stop() if dist.rank == 0 else None
+    t_step_ms = dist.max(total_ms) / args.steps
+    t_main_ms = dist.max(main_ms) / args.steps
+    value = flops_job / (t_step_ms * 1e-3) / 1e12
+
+    # ---- end to end through the public API (pinned host buffers) ---------
+    e2e = None
+    if not args.no_e2e:
+        from paper_2008_11326_b200._lib import check
+
+        lib = load()
+        arrays = [p.wtilde, p.i_eps, p.aqsntemp, p.aqsmtemp]
+        for a in arrays:
+            check(lib.gpp_host_register(a.ctypes.data, a.nbytes), "gpp_host_register")
+        try:
+            h2d = (p.wtilde.nbytes + p.i_eps.nbytes + 16 * nc * (b1 - b0) + 16 * ng * (b1 - b0)
+                   + 8 * args.nw * (b1 - b0))
+            d2h = 8 * 4 * args.nw + 16
+            for _ in range(2):
+                ctx.upload(p, (b0, b1), force=True)
+                ctx.run(args.variant)
+            dist.barrier()
+            dist.sync()
+            t0 = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                ctx.upload(p, (b0, b1), force=True)
+                ctx.run(args.variant)
+            dist.sync()
+            el = time.perf_counter() - t0
+            dist.barrier()
+            el = dist.max(el)
+            e2e = {"value": flops_job / (el / args.e2e_steps) / 1e12, "unit": "TFLOP/s",
+                   "ms_per_step": el / args.e2e_steps * 1e3, "steps": args.e2e_steps,
+                   "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                   "path": "GPPContext.upload(force) + GPPContext.run -> gpp_upload + gpp_run (C ABI)"}
+        finally:
+            for a in arrays:
+                lib.gpp_host_unregister(a.ctypes.data)
+
+    if dist.rank != 0:
+        ctx.close()
+        return
+
+    # ---- CPU baseline (rank 0, N=1 only) ---------------------------------
+    cpu = None
+    if dist.world == 1 and not args.no_cpu_baseline:
+        igp_per_step = 6
+        steps = -(-ng // igp_per_step)  # one full pass over the workload
+        fl, secs = cpu_reference_steps(p, steps, 1, igp_per_step)
+        cpu = {"value": fl / secs / 1e12, "unit": "TFLOP/s", "cores": _cpu_threads(), "kind": "port",
+               "sample": f"one full pass of the {dims} nw={args.nw} workload through the reference's "
+                         f"evaluate_variant('rcp_sq') restated in oracle/ (numpy + OpenBLAS ZGEMM), "
+                         f"in {steps} igp slices of {igp_per_step}; {secs:.2f} s",
+               "cpu_count": os.cpu_count()}
+
+    prof = load_profile_summary() or {}
+    achieved = flops_job / dist.world / (t_main_ms * 1e-3) / 1e12  # dominant kernel, per GPU
+    tot_inst = args.nw * nb * ng * nc
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "TFLOP/s",
+        "n_gpus": dist.world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_step_ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": f"synthetic (synth_problem seed {args.seed}, PCG64 as the reference draws it)",
+        "config": _config(args, dims),
+        "roofline": {
+            "bound": "fp64",
+            "achieved": achieved,
+            "peak": peak_tf,
+            "unit": "TFLOP/s",
+            "frac": achieved / peak_tf,
+            "traffic": prof.get("dram_bytes_per_launch"),
+            "peak_source": "measured live: DFMA microbenchmark (gpp_fp64_peak) on this GPU in this run",
+            "kernel": "gpp_main_kernel<FastPolicy>",
+            "kernel_ms": t_main_ms,
+            "algorithmic_flops_per_launch": flops_job / dist.world,
+            "fma_ratio_analytic": None,
+        },
+        "pct_fp64_peak": 100.0 * value / dist.world / peak_tf,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "branch_stats": {"instances": tot_inst, "near": near, "far": far},
+        "kernel_info": info,
+        "ncu": {k: prof.get(k) for k in ("executed_flops_per_launch", "executed_over_algorithmic",
+                                         "fma_ratio", "source")} if prof else None,
+    }
+    from paper_2008_11326_b200.counters import BranchStats, counters_from_stats, fma_ratio
+
+    cnt = counters_from_stats("rcp_sq", BranchStats(tot_inst, near, far), nb * ng * nc, True)
+    r = fma_ratio(cnt)
+    line["roofline"]["fma_ratio_analytic"] = r
+    line["fma_ceiling_tflops"] = peak_tf * (1 + r) / 2
+    line["pct_fma_ceiling"] = 100.0 * value / dist.world / line["fma_ceiling_tflops"]
+    if args.variant == "rcp_sq":
+        line["parity"] = golden_parity(result, args.workload, args.seed, args.nw)
+    print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def main():
+    args = parse_args()
+    dist = Dist(args.gpus)
+    try:
+        if args.impl == "reference":
+            run_reference(args, dist)
+        else:
+            run_ours(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,23 @@
+"""Minimal driver for ncu: one warm-up and one profiled evaluation.
+
+usage: python tools/profile_run.py [nbands ngpown ncouls] [--nw 3] [--seed 1] [--variant rcp_sq] [--reps 2]
+"""
+import argparse
+import sys
+
+sys.path.insert(0, ".")
+from paper_2008_11326_b200 import GPPContext, synth_problem
+
+ap = argparse.ArgumentParser()
+ap.add_argument("dims", nargs="*", type=int, default=[512, 66, 32768])
+ap.add_argument("--nw", type=int, default=3)
+ap.add_argument("--seed", type=int, default=1)
+ap.add_argument("--variant", default="rcp_sq")
+ap.add_argument("--reps", type=int, default=2)
+a = ap.parse_args()
+p = synth_problem(*a.dims, seed=a.seed, nw=a.nw, check=False)
+ctx = GPPContext(0)
+ctx.upload(p)
+for _ in range(a.reps):
+    r, nf, ms = ctx.run(a.variant)
+print(a.variant, a.dims, "nw", a.nw, "near/far", nf, f"{ms:.3f} ms", r.achtemp)
