@@ -20,7 +20,8 @@
 //   IGP_T (ig, igp) states live in registers; the band loop runs innermost
 //   with aqsmtemp[igp tile, band chunk] and wx[band chunk, :] staged in shared
 //   memory (uniform broadcast reads); aqsntemp[ig, band] is streamed from
-//   global with a one-band register prefetch.  Items are ordered igp-tile
+//   global through a per-thread cp.async ring kAnDepth bands deep, so its
+//   latency is covered without holding prefetched values in registers.  Items are ordered igp-tile
 //   fastest, so the CTAs resident at one time share the same aqsntemp tile
 //   through L2.
 //   iw is innermost: t and eps*t are formed once per (band, igp, ig) and
@@ -36,6 +37,7 @@ constexpr int kThreads = 256;     // threads per CTA (= ig per item)
 constexpr int kMaxChunk = 64;     // bands per item (upper bound)
 constexpr int kMaxIgpTile = 4;    // igp per thread (upper bound)
 constexpr int kMaxNwGroup = 4;    // frequencies per launch (host loops groups)
+constexpr int kAnDepth = 4;       // aqsntemp bands in flight per thread (cp.async ring)
 
 struct Params {
   const double2* wtilde;   // (ncouls, ngpown) F-order
@@ -84,6 +86,20 @@ __device__ __forceinline__ double sqrt_refined(double x) {
   return fma(res, h, g);
 }
 
+// cp.async (LDGSTS) of one 16-byte aqsntemp element into this thread's slot
+// of the shared-memory ring.  Each thread only ever reads the slots it filled
+// itself, so cp.async.wait_group alone orders the copy before the read; no
+// CTA barrier is needed.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // Bit pattern of 1e24: |delw|^2 > 1e-24  <=>  d / |wt|^2 < 1e24.
 constexpr unsigned long long kBits1e24 = 0x44EA784379D99DB4ull;
 
@@ -98,21 +114,86 @@ struct Acc {
   unsigned nn, nf;
 };
 
+// Branch selection shared by the fast formulations.  Decisions are integer
+// compares on the bit patterns of non-negative doubles (ALU pipe, not the
+// FP64 pipe):
+//   near <=> bits(d) > bits(qn)
+//   far  <=> !near && bits(x) - 1 < bits(1e24) - 1      (x in (0, 1e24))
+// Both branch bodies are computed for every instance and only their scalar
+// multipliers are selected -- no divergence.  (PTX selp keeps ptxas from
+// turning the far select into a branch.)
+template <bool COUNT, int NW>
+__device__ __forceinline__ void select_branches(double d, long long qbits, double x, double inv,
+                                                double g, double& in, double& gf, Acc<NW>& acc) {
+  const long long dbits = __double_as_longlong(d);
+  const long long xbits = __double_as_longlong(x);
+  if constexpr (COUNT) {
+    asm("{\n\t.reg .pred pn, pf;\n\t.reg .u64 xm1;\n\t"
+        "setp.gt.s64 pn, %4, %5;\n\t"
+        "sub.u64 xm1, %6, 1;\n\t"
+        "setp.lt.and.u64 pf, xm1, %7, !pn;\n\t"
+        "selp.f64 %0, %8, 0d0000000000000000, pn;\n\t"
+        "selp.f64 %1, %9, 0d0000000000000000, pf;\n\t"
+        "@pn add.u32 %2, %2, 1;\n\t"
+        "@pf add.u32 %3, %3, 1;\n\t}"
+        : "=d"(in), "=d"(gf), "+r"(acc.nn), "+r"(acc.nf)
+        : "l"(dbits), "l"(qbits), "l"(xbits), "l"(kBits1e24 - 1ull), "d"(inv), "d"(g));
+  } else {
+    asm("{\n\t.reg .pred pn, pf;\n\t.reg .u64 xm1;\n\t"
+        "setp.gt.s64 pn, %2, %3;\n\t"
+        "sub.u64 xm1, %4, 1;\n\t"
+        "setp.lt.and.u64 pf, xm1, %5, !pn;\n\t"
+        "selp.f64 %0, %6, 0d0000000000000000, pn;\n\t"
+        "selp.f64 %1, %7, 0d0000000000000000, pf;\n\t}"
+        : "=d"(in), "=d"(gf)
+        : "l"(dbits), "l"(qbits), "l"(xbits), "l"(kBits1e24 - 1ull), "d"(inv), "d"(g));
+  }
+}
+
+// sqrt(x) from the MUFU.RSQ64H seed r (rel. error ~2^-20, measured).
+//   STEPS = 1: one coupled Newton step            4 FP64, rel. error ~1e-12
+//   STEPS = 2: two coupled Newton steps           7 FP64, ~1 ulp
+//   STEPS = 3: one cubic step r (1 + e/2 + 3e^2/8), e = 1 - x r^2,
+//              then sqrt = x r                    5 FP64, ~1 ulp
+template <int STEPS>
+__device__ __forceinline__ double sqrt_nr(double x) {
+  const double r = rsqrt_approx(x);
+  if constexpr (STEPS == 3) {
+    const double t = x * r;                 // sqrt(x) (1 + O(e))
+    const double e = fma(-t, r, 1.0);
+    const double p = fma(e, 0.375, 0.5);
+    const double q = e * p;
+    return fma(t, q, t);
+  } else {
+    double g = x * r;
+    double h = 0.5 * r;
+    double e = fma(-g, h, 0.5);
+    g = fma(g, e, g);
+    if constexpr (STEPS >= 2) {
+      h = fma(h, e, h);
+      double res = fma(-g, g, x);
+      g = fma(res, h, g);
+    }
+    return g;
+  }
+}
+
 // RCP_SQ, optimised (the paper's v8 re-derived for Blackwell).
 //   d     = |wdiff|^2 = (wx - wt.re)^2 + wt.im^2          (1 DADD + 1 DFMA)
 //   inv   = 1/d                                          (MUFU + 3 DFMA)
-//   num   = wt * conj(wdiff) = (wt.re*wdiff.re - wt.im^2, wt.im*wx)
+//   num   = wt * conj(wdiff) = wx * wt - |wt|^2
 //   delw  = num * inv,  |delw|^2 = |wt|^2 / d
 //   near  <=> d > 0.25  &&  |wt|^2 < 4 d  <=>  d > max(0.25, |wt|^2/4) = qn
 //   far   <=> !near && d/|wt|^2 < 1e24
 //   sum a += near * inv * num * (eps t)                   -> ach = a/2
 //   sum b += far  * sqrt(d/|wt|^2) * (eps t)              -> asx = a - b/4
-// Branch decisions are exact integer compares on the bit patterns of
-// non-negative doubles (ALU pipe, not the FP64 pipe); the branch bodies are
-// evaluated for every instance and selected (no divergence).
-struct FastPolicy {
+// ALG 0 forms y = num * (eps t) per instance (6 FP64);  ALG 1 forms
+// P = wt*(eps t) and Q = |wt|^2 (eps t) once per (band, igp, ig) and then
+// y = wx P - Q per instance (2 DFMA), which pays off from nw = 2 on.
+template <int ALG, int SQRT_STEPS>
+struct FastPolicyT {
   struct St {
-    double wtr, wti, wti2, qn, iwt2, er, ei;
+    double wtr, wti, wti2, wt2, qn, iwt2, er, ei;
   };
   static constexpr bool kFast = true;
 
@@ -121,45 +202,55 @@ struct FastPolicy {
     s.wtr = wt.x;
     s.wti = wt.y;
     s.wti2 = wt.y * wt.y;
-    double wt2 = fma(wt.x, wt.x, s.wti2);
-    s.qn = valid ? fmax(0.25, 0.25 * wt2) : __longlong_as_double(0x7FF0000000000000ll);
-    s.iwt2 = valid ? 1.0 / wt2 : __longlong_as_double(0x7FF0000000000000ll);
+    s.wt2 = fma(wt.x, wt.x, s.wti2);
+    s.qn = valid ? fmax(0.25, 0.25 * s.wt2) : __longlong_as_double(0x7FF0000000000000ll);
+    s.iwt2 = valid ? 1.0 / s.wt2 : __longlong_as_double(0x7FF0000000000000ll);
     s.er = valid ? e.x : 0.0;
     s.ei = valid ? e.y : 0.0;
     return s;
   }
 
-  template <int NW>
+  template <int NW, bool COUNT>
   __device__ __forceinline__ static void tuple(const St& s, double tr, double ti,
                                                const double (&wx)[NW], Acc<NW>& acc) {
     // eps * t, shared by every frequency.
     const double etr = fma(s.er, tr, -s.ei * ti);
     const double eti = fma(s.er, ti, s.ei * tr);
+    const long long qbits = __double_as_longlong(s.qn);
+    double pr = 0.0, pi = 0.0, qr = 0.0, qi = 0.0;
+    if constexpr (ALG == 1) {
+      pr = fma(s.wtr, etr, -s.wti * eti);
+      pi = fma(s.wtr, eti, s.wti * etr);
+      qr = s.wt2 * etr;
+      qi = s.wt2 * eti;
+    }
 #pragma unroll
     for (int iw = 0; iw < NW; ++iw) {
       const double wdre = wx[iw] - s.wtr;
       const double d = fma(wdre, wdre, s.wti2);
       const double inv = rcp_refined(d);
-      const double nre = fma(s.wtr, wdre, -s.wti2);
-      const double nim = s.wti * wx[iw];
-      const bool near = __double_as_longlong(d) > __double_as_longlong(s.qn);
       const double x = d * s.iwt2;
-      const bool far = !near && (static_cast<unsigned long long>(__double_as_longlong(x)) - 1ull) <
-                                    (kBits1e24 - 1ull);
-      const double yre = fma(nre, etr, -nim * eti);
-      const double yim = fma(nre, eti, nim * etr);
-      const double in = near ? inv : 0.0;
+      double yre, yim;
+      if constexpr (ALG == 1) {
+        yre = fma(wx[iw], pr, -qr);
+        yim = fma(wx[iw], pi, -qi);
+      } else {
+        const double nre = fma(s.wtr, wdre, -s.wti2);
+        const double nim = s.wti * wx[iw];
+        yre = fma(nre, etr, -nim * eti);
+        yim = fma(nre, eti, nim * etr);
+      }
+      const double g = sqrt_nr<SQRT_STEPS>(x);
+      double in, gf;
+      select_branches<COUNT>(d, qbits, x, inv, g, in, gf, acc);
       acc.a[iw].x = fma(in, yre, acc.a[iw].x);
       acc.a[iw].y = fma(in, yim, acc.a[iw].y);
-      const double g = sqrt_refined(x);
-      const double gf = far ? g : 0.0;
       acc.b[iw].x = fma(gf, etr, acc.b[iw].x);
       acc.b[iw].y = fma(gf, eti, acc.b[iw].y);
-      acc.nn += near;
-      acc.nf += far;
     }
   }
 };
+using FastPolicy = FastPolicyT<1, 3>;
 
 // DIV / RCP / RCP_SQ "as written": the reference's per-instance formulas
 // (kernel.py:68-95) with IEEE division and sqrt, both branch bodies and two
@@ -184,7 +275,7 @@ struct PlainPolicy {
     return s;
   }
 
-  template <int NW>
+  template <int NW, bool COUNT>
   __device__ __forceinline__ static void tuple(const St& s, double tr, double ti,
                                                const double (&wx)[NW], Acc<NW>& acc) {
 #pragma unroll
@@ -244,8 +335,10 @@ struct PlainPolicy {
       acc.a[iw].y += schr * ti + schi * tr;
       acc.b[iw].x += ssxr * tr - ssxi * ti;
       acc.b[iw].y += ssxr * ti + ssxi * tr;
-      acc.nn += near;
-      acc.nf += far;
+      if (COUNT) {
+        acc.nn += near;
+        acc.nf += far;
+      }
     }
   }
 };
@@ -253,12 +346,13 @@ struct PlainPolicy {
 // ---------------------------------------------------------------------------
 // Main kernel.
 // ---------------------------------------------------------------------------
-template <class P, int NW, int IGP_T>
-__global__ void __launch_bounds__(kThreads, 2) gpp_main_kernel(const Params p) {
+template <class P, int NW, int IGP_T, bool COUNT, int MINB = 2>
+__global__ void __launch_bounds__(kThreads, MINB) gpp_main_kernel(const Params p) {
   __shared__ double2 s_am[kMaxChunk][IGP_T];
   __shared__ double s_wx[kMaxChunk][NW];
   __shared__ double s_red[kThreads / 32][4 * NW];
   __shared__ unsigned long long s_cred[kThreads / 32][2];
+  __shared__ __align__(16) double2 s_an[kAnDepth][kThreads];
 
   Acc<NW> acc;
 #pragma unroll
@@ -305,10 +399,17 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_main_kernel(const Params p) {
     __syncthreads();
 
     const double2* anp = p.aqsn + static_cast<size_t>(b0) * p.ncouls + igc;
-    double2 an_next = __ldg(anp);
+#pragma unroll
+    for (int s = 0; s < kAnDepth - 1; ++s) {
+      if (s < nb) cp_async16(&s_an[s][tid], anp + static_cast<size_t>(s) * p.ncouls);
+      cp_async_commit();
+    }
     for (int bb = 0; bb < nb; ++bb) {
-      const double2 an = an_next;
-      if (bb + 1 < nb) an_next = __ldg(anp + static_cast<size_t>(bb + 1) * p.ncouls);
+      const int pf = bb + kAnDepth - 1;
+      if (pf < nb) cp_async16(&s_an[pf % kAnDepth][tid], anp + static_cast<size_t>(pf) * p.ncouls);
+      cp_async_commit();
+      cp_async_wait<kAnDepth - 1>();
+      const double2 an = s_an[bb % kAnDepth][tid];
       double wx[NW];
 #pragma unroll
       for (int iw = 0; iw < NW; ++iw) wx[iw] = s_wx[bb][iw];
@@ -318,9 +419,10 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_main_kernel(const Params p) {
         // t = an * conj(am)
         const double tr = fma(an.x, am.x, an.y * am.y);
         const double ti = fma(an.y, am.x, -an.x * am.y);
-        P::template tuple<NW>(st[j], tr, ti, wx, acc);
+        P::template tuple<NW, COUNT>(st[j], tr, ti, wx, acc);
       }
     }
+    cp_async_wait<0>();
   }
 
   // Deterministic block reduction: warp xor-tree, then warps in order.
@@ -353,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_main_kernel(const Params p) {
 #pragma unroll
     for (int w = 0; w < kThreads / 32; ++w) s += s_red[w][tid];
     p.partials[static_cast<size_t>(blockIdx.x) * (4 * NW) + tid] = s;
-  } else if (tid < 4 * NW + 2) {
+  } else if (COUNT && tid < 4 * NW + 2) {
     const int c = tid - 4 * NW;
     unsigned long long s = 0;
 #pragma unroll
@@ -369,7 +471,8 @@ template <int NW>
 __global__ void __launch_bounds__(256) gpp_finalize_kernel(const double* partials,
                                                            const unsigned long long* cpartials,
                                                            int nparts, int nw_total, int iw0,
-                                                           int fast, int first, double* out,
+                                                           int fast, int first, int counted,
+                                                           double* out,
                                                            unsigned long long* counts) {
   __shared__ double s[256];
   __shared__ unsigned long long sc[256];
@@ -387,8 +490,8 @@ __global__ void __launch_bounds__(256) gpp_finalize_kernel(const double* partial
     sum[k] = s[0];
     __syncthreads();
   }
-  unsigned long long csum[2];
-  for (int c = 0; c < 2; ++c) {
+  unsigned long long csum[2] = {0ull, 0ull};
+  for (int c = 0; c < 2 && counted; ++c) {
     unsigned long long acc = 0;
     for (int i = tid; i < nparts; i += 256) acc += cpartials[static_cast<size_t>(i) * 2 + c];
     sc[tid] = acc;

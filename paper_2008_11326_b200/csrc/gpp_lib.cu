@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -140,38 +141,82 @@ struct Plan {
 
 using KernelFn = void (*)(gpp::Params);
 
-template <int NW>
-KernelFn pick_fast(int igp_t) {
-  if (NW >= 4 || igp_t == 3) return gpp::gpp_main_kernel<gpp::FastPolicy, NW, 3>;
-  return gpp::gpp_main_kernel<gpp::FastPolicy, NW, (NW >= 4 ? 3 : 4)>;
+// Tuning override for experiments: GPP_TUNE="igp,minb,alg,sqrt" selects an
+// alternative register/occupancy trade-off and formulation of the fast kernel
+// (nw 2 or 3 only; 0 keeps the default).
+struct Tune {
+  int igp = 0, minb = 0, alg = -1, sq = 0;
+};
+Tune read_tune() {
+  Tune t;
+  const char* e = std::getenv("GPP_TUNE");
+  if (e) std::sscanf(e, "%d,%d,%d,%d", &t.igp, &t.minb, &t.alg, &t.sq);
+  return t;
 }
 
-template <class P>
+template <class FP, int NW, bool C>
+KernelFn pick_fast_tuned(const Tune& t) {
+  if (t.minb == 3) {
+    if (t.igp == 2) return gpp::gpp_main_kernel<FP, NW, 2, C, 3>;
+    return gpp::gpp_main_kernel<FP, NW, 3, C, 3>;
+  }
+  if (t.igp == 2) return gpp::gpp_main_kernel<FP, NW, 2, C>;
+  if (t.igp == 4) return gpp::gpp_main_kernel<FP, NW, 4, C>;
+  return gpp::gpp_main_kernel<FP, NW, 3, C>;
+}
+
+template <int NW, bool C>
+KernelFn pick_fast(int igp_t) {
+  if constexpr (NW == 2 || NW == 3) {
+    const Tune t = read_tune();
+    if (t.alg >= 0 || t.minb || t.igp) {
+      if (t.alg == 1 && t.sq == 1) return pick_fast_tuned<gpp::FastPolicyT<1, 1>, NW, C>(t);
+      if (t.alg == 1 && t.sq == 2) return pick_fast_tuned<gpp::FastPolicyT<1, 2>, NW, C>(t);
+      if (t.alg == 1) return pick_fast_tuned<gpp::FastPolicyT<1, 3>, NW, C>(t);
+      if (t.sq == 1) return pick_fast_tuned<gpp::FastPolicyT<0, 1>, NW, C>(t);
+      if (t.sq == 2) return pick_fast_tuned<gpp::FastPolicyT<0, 2>, NW, C>(t);
+      return pick_fast_tuned<gpp::FastPolicyT<0, 3>, NW, C>(t);
+    }
+  }
+  if (NW >= 4 || igp_t == 3) return gpp::gpp_main_kernel<gpp::FastPolicy, NW, 3, C>;
+  return gpp::gpp_main_kernel<gpp::FastPolicy, NW, (NW >= 4 ? 3 : 4), C>;
+}
+
+template <class P, bool C>
 KernelFn pick_plain(int nw) {
   switch (nw) {
-    case 1: return gpp::gpp_main_kernel<P, 1, 2>;
-    case 2: return gpp::gpp_main_kernel<P, 2, 2>;
-    case 3: return gpp::gpp_main_kernel<P, 3, 2>;
-    default: return gpp::gpp_main_kernel<P, 4, 2>;
+    case 1: return gpp::gpp_main_kernel<P, 1, 2, C>;
+    case 2: return gpp::gpp_main_kernel<P, 2, 2, C>;
+    case 3: return gpp::gpp_main_kernel<P, 3, 2, C>;
+    default: return gpp::gpp_main_kernel<P, 4, 2, C>;
   }
 }
 
-KernelFn pick_kernel(int variant, int nw, int igp_t) {
+template <bool C>
+KernelFn pick_kernel_c(int variant, int nw, int igp_t) {
   switch (variant) {
-    case GPP_VARIANT_DIV: return pick_plain<gpp::PlainPolicy<0>>(nw);
-    case GPP_VARIANT_RCP: return pick_plain<gpp::PlainPolicy<1>>(nw);
+    case GPP_VARIANT_DIV: return pick_plain<gpp::PlainPolicy<0>, C>(nw);
+    case GPP_VARIANT_RCP: return pick_plain<gpp::PlainPolicy<1>, C>(nw);
     default:
       switch (nw) {
-        case 1: return pick_fast<1>(igp_t);
-        case 2: return pick_fast<2>(igp_t);
-        case 3: return pick_fast<3>(igp_t);
-        default: return pick_fast<4>(igp_t);
+        case 1: return pick_fast<1, C>(igp_t);
+        case 2: return pick_fast<2, C>(igp_t);
+        case 3: return pick_fast<3, C>(igp_t);
+        default: return pick_fast<4, C>(igp_t);
       }
   }
 }
 
+// count: whether the kernel also produces the near/far branch counts (the
+// reference's branch_stats, kernel.py:130-137).  The uncounted kernel is the
+// evaluate_variant path; the counted one costs two predicated integer adds
+// per instance.
+KernelFn pick_kernel(int variant, int nw, int igp_t, bool count) {
+  return count ? pick_kernel_c<true>(variant, nw, igp_t) : pick_kernel_c<false>(variant, nw, igp_t);
+}
+
 using FinalizeFn = void (*)(const double*, const unsigned long long*, int, int, int, int, int,
-                            double*, unsigned long long*);
+                            int, double*, unsigned long long*);
 FinalizeFn pick_finalize(int nw) {
   switch (nw) {
     case 1: return gpp::gpp_finalize_kernel<1>;
@@ -191,7 +236,7 @@ int choose_igp_tile(int64_t ngpown) {
   return best;
 }
 
-int make_plan(gpp_ctx* c, int variant, int nw_group, Plan* pl) {
+int make_plan(gpp_ctx* c, int variant, int nw_group, bool count, Plan* pl) {
   // The plain (as-written) variants keep two igp per thread and the fast
   // kernel drops to 3 at four frequencies: both choices avoid spills under
   // the 128-register budget of __launch_bounds__(256, 2).
@@ -199,9 +244,13 @@ int make_plan(gpp_ctx* c, int variant, int nw_group, Plan* pl) {
     pl->igp_t = 2;
   else
     pl->igp_t = nw_group >= 4 ? 3 : choose_igp_tile(c->ngpown);
+  const Tune tune = read_tune();
+  if (variant == GPP_VARIANT_RCP_SQ && (nw_group == 2 || nw_group == 3) && tune.igp >= 2 &&
+      tune.igp <= 4)
+    pl->igp_t = tune.igp;
   pl->n_igblk = static_cast<int>((c->ncouls + gpp::kThreads - 1) / gpp::kThreads);
   pl->n_igptile = static_cast<int>((c->ngpown + pl->igp_t - 1) / pl->igp_t);
-  KernelFn fn = pick_kernel(variant, nw_group, pl->igp_t);
+  KernelFn fn = pick_kernel(variant, nw_group, pl->igp_t, count);
   int bps = 0;
   GPP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, gpp::kThreads, 0));
   cudaFuncAttributes attr;
@@ -231,14 +280,14 @@ int nw_groups(int nw, std::vector<std::pair<int, int>>* groups) {
 
 // Enqueue one full evaluation on c->stream.  If ev_main is non-null, the
 // main kernels of all frequency groups are bracketed by ev_main[0..1].
-int enqueue_eval(gpp_ctx* c, int variant, cudaEvent_t* ev_main, bool allreduce) {
+int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool allreduce) {
   std::vector<std::pair<int, int>> groups;
   nw_groups(c->nw, &groups);
   bool first = true;
   for (size_t gi = 0; gi < groups.size(); ++gi) {
     const int iw0 = groups[gi].first, nwg = groups[gi].second;
     Plan pl;
-    int rc = make_plan(c, variant, nwg, &pl);
+    int rc = make_plan(c, variant, nwg, count, &pl);
     if (rc) return rc;
     GPP_CUDA(c->partials.ensure(static_cast<size_t>(pl.grid) * 4 * gpp::kMaxNwGroup));
     GPP_CUDA(c->cpartials.ensure(static_cast<size_t>(pl.grid) * 2));
@@ -259,14 +308,15 @@ int enqueue_eval(gpp_ctx* c, int variant, cudaEvent_t* ev_main, bool allreduce) 
     p.n_items = pl.n_items;
     p.partials = c->partials.ptr;
     p.cpartials = c->cpartials.ptr;
-    KernelFn fn = pick_kernel(variant, nwg, pl.igp_t);
+    KernelFn fn = pick_kernel(variant, nwg, pl.igp_t, count);
     if (ev_main && gi == 0) GPP_CUDA(cudaEventRecord(ev_main[0], c->stream));
     fn<<<pl.grid, gpp::kThreads, 0, c->stream>>>(p);
     GPP_CUDA(cudaGetLastError());
     if (ev_main && gi + 1 == groups.size()) GPP_CUDA(cudaEventRecord(ev_main[1], c->stream));
     pick_finalize(nwg)<<<1, 256, 0, c->stream>>>(c->partials.ptr, c->cpartials.ptr, pl.grid,
                                                   c->nw, iw0, variant == GPP_VARIANT_RCP_SQ,
-                                                  first ? 1 : 0, c->out.ptr, c->counts.ptr);
+                                                  first ? 1 : 0, count ? 1 : 0, c->out.ptr,
+                                                  c->counts.ptr);
     GPP_CUDA(cudaGetLastError());
     first = false;
   }
@@ -423,7 +473,7 @@ int gpp_run(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp, int64
   DeviceGuard g(c->device);
   if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
   GPP_CUDA(cudaEventRecord(c->ev[2], c->stream));
-  rc = enqueue_eval(c, variant, nullptr, false);
+  rc = enqueue_eval(c, variant, near_far != nullptr, nullptr, false);
   if (rc) return rc;
   GPP_CUDA(cudaEventRecord(c->ev[3], c->stream));
   if (c->comm && c->nranks > 1) {
@@ -464,7 +514,7 @@ int gpp_time(gpp_ctx* c, int32_t variant, int32_t iters, float* total_ms, float*
     cudaError_t e = cudaEventRecord(c->ev[2], c->stream);
     if (e != cudaSuccess) { result = cuda_fail(e, "cudaEventRecord"); break; }
     for (int i = 0; i < iters && result == GPP_OK; ++i)
-      result = enqueue_eval(c, variant, &evs[2 * static_cast<size_t>(i)], true);
+      result = enqueue_eval(c, variant, false, &evs[2 * static_cast<size_t>(i)], true);
     if (result) break;
     e = cudaEventRecord(c->ev[3], c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
@@ -493,7 +543,7 @@ int gpp_kernel_info(gpp_ctx* c, int32_t variant, int32_t* registers_per_thread,
   DeviceGuard g(c->device);
   if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
   Plan pl;
-  rc = make_plan(c, variant, std::min(c->nw, gpp::kMaxNwGroup), &pl);
+  rc = make_plan(c, variant, std::min(c->nw, gpp::kMaxNwGroup), false, &pl);
   if (rc) return rc;
   if (registers_per_thread) *registers_per_thread = pl.regs;
   if (threads_per_block) *threads_per_block = gpp::kThreads;
