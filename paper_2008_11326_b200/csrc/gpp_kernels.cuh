@@ -49,6 +49,7 @@ struct Params {
   int nw_total, iw0;       // this launch evaluates iw in [iw0, iw0 + NW)
   int n_igblk, n_igptile, bchunk;
   long long n_items;
+  double wxmax;            // max |wx| over the uploaded bands (regular-item guard)
   double* partials;                 // [gridDim.x][4 * NW]
   unsigned long long* cpartials;    // [gridDim.x][2]
 };
@@ -150,6 +151,53 @@ __device__ __forceinline__ void select_branches(double d, long long qbits, doubl
   }
 }
 
+// Seed selection (ALG 2): the branch decisions gate the MUFU seeds instead of
+// the refined results.  A zero seed refines to exactly zero (e = 1 - d*0 = 1,
+// r = 0 * (...) = 0), so selecting the seed's high word (the low word of a
+// MUFU.RCP64H / RSQ64H result is zero) costs one 32-bit select per branch
+// instead of a 64-bit select of the refined value.
+template <bool COUNT, int NW>
+__device__ __forceinline__ void gated_seeds(double d, long long qbits, double x, double& rr,
+                                            double& rs, Acc<NW>& acc) {
+  const long long dbits = __double_as_longlong(d);
+  const long long xbits = __double_as_longlong(x);
+  if constexpr (COUNT) {
+    asm("{\n\t.reg .pred pn, pf;\n\t.reg .u64 xm1;\n\t.reg .f64 s0, s1;\n\t"
+        ".reg .b32 l0, h0, l1, h1;\n\t"
+        "setp.gt.s64 pn, %4, %5;\n\t"
+        "sub.u64 xm1, %6, 1;\n\t"
+        "setp.lt.and.u64 pf, xm1, %7, !pn;\n\t"
+        "rcp.approx.ftz.f64 s0, %8;\n\t"
+        "rsqrt.approx.ftz.f64 s1, %9;\n\t"
+        "mov.b64 {l0, h0}, s0;\n\t"
+        "mov.b64 {l1, h1}, s1;\n\t"
+        "selp.b32 h0, h0, 0, pn;\n\t"
+        "selp.b32 h1, h1, 0, pf;\n\t"
+        "mov.b64 %0, {l0, h0};\n\t"
+        "mov.b64 %1, {l1, h1};\n\t"
+        "@pn add.u32 %2, %2, 1;\n\t"
+        "@pf add.u32 %3, %3, 1;\n\t}"
+        : "=d"(rr), "=d"(rs), "+r"(acc.nn), "+r"(acc.nf)
+        : "l"(dbits), "l"(qbits), "l"(xbits), "l"(kBits1e24 - 1ull), "d"(d), "d"(x));
+  } else {
+    asm("{\n\t.reg .pred pn, pf;\n\t.reg .u64 xm1;\n\t.reg .f64 s0, s1;\n\t"
+        ".reg .b32 l0, h0, l1, h1;\n\t"
+        "setp.gt.s64 pn, %2, %3;\n\t"
+        "sub.u64 xm1, %4, 1;\n\t"
+        "setp.lt.and.u64 pf, xm1, %5, !pn;\n\t"
+        "rcp.approx.ftz.f64 s0, %6;\n\t"
+        "rsqrt.approx.ftz.f64 s1, %7;\n\t"
+        "mov.b64 {l0, h0}, s0;\n\t"
+        "mov.b64 {l1, h1}, s1;\n\t"
+        "selp.b32 h0, h0, 0, pn;\n\t"
+        "selp.b32 h1, h1, 0, pf;\n\t"
+        "mov.b64 %0, {l0, h0};\n\t"
+        "mov.b64 %1, {l1, h1};\n\t}"
+        : "=d"(rr), "=d"(rs)
+        : "l"(dbits), "l"(qbits), "l"(xbits), "l"(kBits1e24 - 1ull), "d"(d), "d"(x));
+  }
+}
+
 // sqrt(x) from the MUFU.RSQ64H seed r (rel. error ~2^-20, measured).
 //   STEPS = 1: one coupled Newton step            4 FP64, rel. error ~1e-12
 //   STEPS = 2: two coupled Newton steps           7 FP64, ~1 ulp
@@ -187,15 +235,19 @@ __device__ __forceinline__ double sqrt_nr(double x) {
 //   far   <=> !near && d/|wt|^2 < 1e24
 //   sum a += near * inv * num * (eps t)                   -> ach = a/2
 //   sum b += far  * sqrt(d/|wt|^2) * (eps t)              -> asx = a - b/4
-// ALG 0 forms y = num * (eps t) per instance (6 FP64);  ALG 1 forms
+// ALG 0 forms y = num * (eps t) per instance (6 FP64);  ALG 1/2 form
 // P = wt*(eps t) and Q = |wt|^2 (eps t) once per (band, igp, ig) and then
 // y = wx P - Q per instance (2 DFMA), which pays off from nw = 2 on.
+// ALG 2 additionally gates the MUFU seeds (gated_seeds) instead of selecting
+// the refined multipliers.
 template <int ALG, int SQRT_STEPS>
 struct FastPolicyT {
   struct St {
     double wtr, wti, wti2, wt2, qn, iwt2, er, ei;
   };
   static constexpr bool kFast = true;
+  static constexpr bool kHasFastPath = false;
+  __device__ __forceinline__ static bool regular(const St&, double) { return false; }
 
   __device__ __forceinline__ static St make(double2 wt, double2 e, bool valid) {
     St s;
@@ -204,13 +256,15 @@ struct FastPolicyT {
     s.wti2 = wt.y * wt.y;
     s.wt2 = fma(wt.x, wt.x, s.wti2);
     s.qn = valid ? fmax(0.25, 0.25 * s.wt2) : __longlong_as_double(0x7FF0000000000000ll);
-    s.iwt2 = valid ? 1.0 / s.wt2 : __longlong_as_double(0x7FF0000000000000ll);
+    // x = d * iwt2 must be 0 (never far) on padded lanes and for wt = 0
+    // (delw = 0 is degenerate), so those lanes carry iwt2 = 0, not inf.
+    s.iwt2 = (valid && s.wt2 > 0.0) ? 1.0 / s.wt2 : 0.0;
     s.er = valid ? e.x : 0.0;
     s.ei = valid ? e.y : 0.0;
     return s;
   }
 
-  template <int NW, bool COUNT>
+  template <int NW, bool COUNT, bool FAST>
   __device__ __forceinline__ static void tuple(const St& s, double tr, double ti,
                                                const double (&wx)[NW], Acc<NW>& acc) {
     // eps * t, shared by every frequency.
@@ -218,7 +272,7 @@ struct FastPolicyT {
     const double eti = fma(s.er, ti, s.ei * tr);
     const long long qbits = __double_as_longlong(s.qn);
     double pr = 0.0, pi = 0.0, qr = 0.0, qi = 0.0;
-    if constexpr (ALG == 1) {
+    if constexpr (ALG >= 1) {
       pr = fma(s.wtr, etr, -s.wti * eti);
       pi = fma(s.wtr, eti, s.wti * etr);
       qr = s.wt2 * etr;
@@ -228,10 +282,9 @@ struct FastPolicyT {
     for (int iw = 0; iw < NW; ++iw) {
       const double wdre = wx[iw] - s.wtr;
       const double d = fma(wdre, wdre, s.wti2);
-      const double inv = rcp_refined(d);
       const double x = d * s.iwt2;
       double yre, yim;
-      if constexpr (ALG == 1) {
+      if constexpr (ALG >= 1) {
         yre = fma(wx[iw], pr, -qr);
         yim = fma(wx[iw], pi, -qi);
       } else {
@@ -240,9 +293,23 @@ struct FastPolicyT {
         yre = fma(nre, etr, -nim * eti);
         yim = fma(nre, eti, nim * etr);
       }
-      const double g = sqrt_nr<SQRT_STEPS>(x);
       double in, gf;
-      select_branches<COUNT>(d, qbits, x, inv, g, in, gf, acc);
+      if constexpr (ALG == 2) {
+        double rr, rs;
+        gated_seeds<COUNT>(d, qbits, x, rr, rs, acc);
+        // 1/d refined from the gated seed (cubic step), sqrt(x) likewise.
+        double e = fma(-d, rr, 1.0);
+        e = fma(e, e, e);
+        in = fma(e, rr, rr);
+        const double t = x * rs;
+        const double es = fma(-t, rs, 1.0);
+        const double ps = fma(es, 0.375, 0.5);
+        gf = fma(t, es * ps, t);
+      } else {
+        const double inv = rcp_refined(d);
+        const double g = sqrt_nr<SQRT_STEPS>(x);
+        select_branches<COUNT>(d, qbits, x, inv, g, in, gf, acc);
+      }
       acc.a[iw].x = fma(in, yre, acc.a[iw].x);
       acc.a[iw].y = fma(in, yim, acc.a[iw].y);
       acc.b[iw].x = fma(gf, etr, acc.b[iw].x);
@@ -250,7 +317,114 @@ struct FastPolicyT {
     }
   }
 };
-using FastPolicy = FastPolicyT<1, 3>;
+// RCP_SQ, production kernel (ALG 3).  Differences from FastPolicyT:
+//  * One MUFU.RSQ64H seed serves both branches: r = rsqrt(d) refined by one
+//    cubic step gives sqrt(d) = d r and 1/d = r^2 (~1-2 ulp), so an instance
+//    costs one MUFU and 7 FP64 for both reciprocal and square root.
+//  * The far body is sqrt(d) * (|wt|^-1 eps t): the 1/|wt| factor is applied
+//    once per (band, igp, ig) instead of forming x = d/|wt|^2 per instance.
+//  * Regular items: when no instance of an item can be degenerate -- wt.im != 0
+//    (so d > 0) and |wt|^2 > 1e-24 (max|wx| + |wt|)^2 (so |delw| > 1e-12) --
+//    far is exactly !near and the 64-bit far compare disappears.  Items that
+//    are not regular (and the counting kernel) take the general path, which
+//    evaluates the full far test.
+// The optimisations were chosen against the measured register-file read
+// model of the loop (tools/sass_rf.py): the kernel is bound by
+// operand reads, not by the FP64 pipe, so ALU and FP64 instructions both
+// count.
+struct FastPolicy3 {
+  struct St {
+    double wtr, wti, wti2, wt2, qn, rwt, er, ei;
+  };
+  static constexpr bool kFast = true;
+  static constexpr bool kHasFastPath = true;
+
+  __device__ __forceinline__ static St make(double2 wt, double2 e, bool valid) {
+    St s;
+    s.wtr = wt.x;
+    s.wti = wt.y;
+    s.wti2 = wt.y * wt.y;
+    s.wt2 = fma(wt.x, wt.x, s.wti2);
+    s.qn = valid ? fmax(0.25, 0.25 * s.wt2) : __longlong_as_double(0x7FF0000000000000ll);
+    // Padded lanes and wt == 0 carry rwt = 0: never far in the general path
+    // (x = 0) and a zero far term in the regular path.
+    s.rwt = (valid && s.wt2 > 0.0) ? 1.0 / sqrt(s.wt2) : 0.0;
+    s.er = valid ? e.x : 0.0;
+    s.ei = valid ? e.y : 0.0;
+    return s;
+  }
+  // No instance of this (ig, igp) can be degenerate for any wx with
+  // |wx| <= wxmax.  (Padded lanes: qn = inf and eps = 0, so they contribute
+  // nothing on either path.)
+  __device__ __forceinline__ static bool regular(const St& s, double wxmax) {
+    if (s.qn == __longlong_as_double(0x7FF0000000000000ll)) return true;
+    if (s.wti == 0.0) return false;
+    const double m = wxmax + sqrt(s.wt2);
+    return s.wt2 > 1.000001e-24 * m * m;
+  }
+
+  template <int NW, bool COUNT, bool FAST>
+  __device__ __forceinline__ static void tuple(const St& s, double tr, double ti,
+                                               const double (&wx)[NW], Acc<NW>& acc) {
+    const double etr = fma(s.er, tr, -s.ei * ti);
+    const double eti = fma(s.er, ti, s.ei * tr);
+    const double pr = fma(s.wtr, etr, -s.wti * eti);
+    const double pi = fma(s.wtr, eti, s.wti * etr);
+    const double qr = s.wt2 * etr;
+    const double qi = s.wt2 * eti;
+    const long long qbits = __double_as_longlong(s.qn);
+    if constexpr (FAST && !COUNT) {
+      const double efr = s.rwt * etr;
+      const double efi = s.rwt * eti;
+#pragma unroll
+      for (int iw = 0; iw < NW; ++iw) {
+        const double wdre = wx[iw] - s.wtr;
+        const double d = fma(wdre, wdre, s.wti2);
+        const double r = rsqrt_approx(d);
+        const double t = d * r;
+        const double e = fma(-t, r, 1.0);
+        const double pe = fma(e, 0.375, 0.5);
+        const double q = e * pe;
+        const double rr = fma(r, q, r);  // 1/sqrt(d)
+        const double sq = fma(t, q, t);  // sqrt(d)
+        const double inv = rr * rr;      // 1/d
+        const double yre = fma(wx[iw], pr, -qr);
+        const double yim = fma(wx[iw], pi, -qi);
+        double in, gf;
+        asm("{\n\t.reg .pred pn;\n\t"
+            "setp.gt.s64 pn, %2, %3;\n\t"
+            "selp.f64 %0, %4, 0d0000000000000000, pn;\n\t"
+            "selp.f64 %1, 0d0000000000000000, %5, pn;\n\t}"
+            : "=d"(in), "=d"(gf)
+            : "l"(__double_as_longlong(d)), "l"(qbits), "d"(inv), "d"(sq));
+        acc.a[iw].x = fma(in, yre, acc.a[iw].x);
+        acc.a[iw].y = fma(in, yim, acc.a[iw].y);
+        acc.b[iw].x = fma(gf, efr, acc.b[iw].x);
+        acc.b[iw].y = fma(gf, efi, acc.b[iw].y);
+      }
+    } else {
+      const double iwt2 = s.rwt * s.rwt;
+#pragma unroll
+      for (int iw = 0; iw < NW; ++iw) {
+        const double wdre = wx[iw] - s.wtr;
+        const double d = fma(wdre, wdre, s.wti2);
+        const double inv = rcp_refined(d);
+        const double x = d * iwt2;
+        const double yre = fma(wx[iw], pr, -qr);
+        const double yim = fma(wx[iw], pi, -qi);
+        const double g = sqrt_nr<3>(x);
+        double in, gf;
+        select_branches<COUNT>(d, qbits, x, inv, g, in, gf, acc);
+        acc.a[iw].x = fma(in, yre, acc.a[iw].x);
+        acc.a[iw].y = fma(in, yim, acc.a[iw].y);
+        acc.b[iw].x = fma(gf, etr, acc.b[iw].x);
+        acc.b[iw].y = fma(gf, eti, acc.b[iw].y);
+      }
+    }
+  }
+};
+
+using FastPolicy = FastPolicy3;
 
 // DIV / RCP / RCP_SQ "as written": the reference's per-instance formulas
 // (kernel.py:68-95) with IEEE division and sqrt, both branch bodies and two
@@ -264,6 +438,7 @@ struct PlainPolicy {
     bool valid;
   };
   static constexpr bool kFast = false;
+  static constexpr bool kHasFastPath = false;
 
   __device__ __forceinline__ static St make(double2 wt, double2 e, bool valid) {
     St s;
@@ -274,8 +449,9 @@ struct PlainPolicy {
     s.valid = valid;
     return s;
   }
+  __device__ __forceinline__ static bool regular(const St&, double) { return false; }
 
-  template <int NW, bool COUNT>
+  template <int NW, bool COUNT, bool FAST>
   __device__ __forceinline__ static void tuple(const St& s, double tr, double ti,
                                                const double (&wx)[NW], Acc<NW>& acc) {
 #pragma unroll
@@ -346,6 +522,41 @@ struct PlainPolicy {
 // ---------------------------------------------------------------------------
 // Main kernel.
 // ---------------------------------------------------------------------------
+// The band loop of one item: aqsntemp streamed through the per-thread
+// cp.async ring, aqsmtemp / wx read from shared memory (uniform broadcasts).
+template <class P, int NW, int IGP_T, bool COUNT, bool FAST>
+__device__ __forceinline__ void band_loop(const double2* anp, int ncouls, int nb,
+                                          double2 (&s_an)[kAnDepth][kThreads],
+                                          const double2 (&s_am)[kMaxChunk][IGP_T],
+                                          const double (&s_wx)[kMaxChunk][NW],
+                                          const typename P::St (&st)[IGP_T], Acc<NW>& acc) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int s = 0; s < kAnDepth - 1; ++s) {
+    if (s < nb) cp_async16(&s_an[s][tid], anp + static_cast<size_t>(s) * ncouls);
+    cp_async_commit();
+  }
+  for (int bb = 0; bb < nb; ++bb) {
+    const int pf = bb + kAnDepth - 1;
+    if (pf < nb) cp_async16(&s_an[pf % kAnDepth][tid], anp + static_cast<size_t>(pf) * ncouls);
+    cp_async_commit();
+    cp_async_wait<kAnDepth - 1>();
+    const double2 an = s_an[bb % kAnDepth][tid];
+    double wx[NW];
+#pragma unroll
+    for (int iw = 0; iw < NW; ++iw) wx[iw] = s_wx[bb][iw];
+#pragma unroll
+    for (int j = 0; j < IGP_T; ++j) {
+      const double2 am = s_am[bb][j];
+      // t = an * conj(am)
+      const double tr = fma(an.x, am.x, an.y * am.y);
+      const double ti = fma(an.y, am.x, -an.x * am.y);
+      P::template tuple<NW, COUNT, FAST>(st[j], tr, ti, wx, acc);
+    }
+  }
+  cp_async_wait<0>();
+}
+
 template <class P, int NW, int IGP_T, bool COUNT, int MINB = 2>
 __global__ void __launch_bounds__(kThreads, MINB) gpp_main_kernel(const Params p) {
   __shared__ double2 s_am[kMaxChunk][IGP_T];
@@ -384,7 +595,14 @@ __global__ void __launch_bounds__(kThreads, MINB) gpp_main_kernel(const Params p
       st[j] = P::make(__ldg(p.wtilde + off), __ldg(p.eps + off), v);
     }
 
-    __syncthreads();  // previous item finished reading shared memory
+    // Block-uniform choice of the regular (no degenerate instance possible)
+    // fast path; the barrier also orders this item's staging after the
+    // previous item's shared-memory reads.
+    bool thread_regular = true;
+#pragma unroll
+    for (int j = 0; j < IGP_T; ++j) thread_regular = thread_regular && P::regular(st[j], p.wxmax);
+    const bool item_regular =
+        __syncthreads_and(P::kHasFastPath && !COUNT && thread_regular) != 0;
     for (int k = tid; k < nb * IGP_T; k += kThreads) {
       const int bb = k / IGP_T, j = k - bb * IGP_T;
       const int igp = igpt * IGP_T + j;
@@ -399,30 +617,10 @@ __global__ void __launch_bounds__(kThreads, MINB) gpp_main_kernel(const Params p
     __syncthreads();
 
     const double2* anp = p.aqsn + static_cast<size_t>(b0) * p.ncouls + igc;
-#pragma unroll
-    for (int s = 0; s < kAnDepth - 1; ++s) {
-      if (s < nb) cp_async16(&s_an[s][tid], anp + static_cast<size_t>(s) * p.ncouls);
-      cp_async_commit();
-    }
-    for (int bb = 0; bb < nb; ++bb) {
-      const int pf = bb + kAnDepth - 1;
-      if (pf < nb) cp_async16(&s_an[pf % kAnDepth][tid], anp + static_cast<size_t>(pf) * p.ncouls);
-      cp_async_commit();
-      cp_async_wait<kAnDepth - 1>();
-      const double2 an = s_an[bb % kAnDepth][tid];
-      double wx[NW];
-#pragma unroll
-      for (int iw = 0; iw < NW; ++iw) wx[iw] = s_wx[bb][iw];
-#pragma unroll
-      for (int j = 0; j < IGP_T; ++j) {
-        const double2 am = s_am[bb][j];
-        // t = an * conj(am)
-        const double tr = fma(an.x, am.x, an.y * am.y);
-        const double ti = fma(an.y, am.x, -an.x * am.y);
-        P::template tuple<NW, COUNT>(st[j], tr, ti, wx, acc);
-      }
-    }
-    cp_async_wait<0>();
+    if (item_regular)
+      band_loop<P, NW, IGP_T, COUNT, true>(anp, p.ncouls, nb, s_an, s_am, s_wx, st, acc);
+    else
+      band_loop<P, NW, IGP_T, COUNT, false>(anp, p.ncouls, nb, s_an, s_am, s_wx, st, acc);
   }
 
   // Deterministic block reduction: warp xor-tree, then warps in order.
@@ -529,15 +727,18 @@ __global__ void __launch_bounds__(256) gpp_finalize_kernel(const double* partial
   }
 }
 
-// FP64 pipe peak: 8 independent DFMA chains per thread.
+// FP64 pipe peak: 8 independent DFMA chains per thread, a = a * a + c.
+// One register operand per DFMA keeps the operand collector out of the way
+// (a DFMA with three distinct register operands runs at 2/3 rate on B200,
+// measured by tools/fp64_issue_probe.cu), so this measures the FP64 pipe.
 __global__ void __launch_bounds__(256) fp64_peak_kernel(double* sink, int iters, double b,
                                                         double c) {
   double a[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 1e-3 + k;
+  for (int k = 0; k < 8; ++k) a[k] = (threadIdx.x * 1e-3 + k) * b * 1e-4;
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], b, c);
+    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], a[k], c);
   }
   double s = 0.0;
 #pragma unroll

@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -92,6 +93,7 @@ struct gpp_ctx {
   bool have_problem = false;
   int64_t nbands = 0, ngpown = 0, ncouls = 0;
   int nw = 0;
+  double wxmax = 0.0;  // max |wx| over the uploaded shard
 
   DevBuf<double2> wtilde, eps, aqsn, aqsm;
   DevBuf<double> wxb;
@@ -145,12 +147,12 @@ using KernelFn = void (*)(gpp::Params);
 // alternative register/occupancy trade-off and formulation of the fast kernel
 // (nw 2 or 3 only; 0 keeps the default).
 struct Tune {
-  int igp = 0, minb = 0, alg = -1, sq = 0;
+  int igp = 0, minb = 0, alg = -1, sq = 0, bps = 0;
 };
 Tune read_tune() {
   Tune t;
   const char* e = std::getenv("GPP_TUNE");
-  if (e) std::sscanf(e, "%d,%d,%d,%d", &t.igp, &t.minb, &t.alg, &t.sq);
+  if (e) std::sscanf(e, "%d,%d,%d,%d,%d", &t.igp, &t.minb, &t.alg, &t.sq, &t.bps);
   return t;
 }
 
@@ -170,6 +172,8 @@ KernelFn pick_fast(int igp_t) {
   if constexpr (NW == 2 || NW == 3) {
     const Tune t = read_tune();
     if (t.alg >= 0 || t.minb || t.igp) {
+      if (t.alg == 3) return pick_fast_tuned<gpp::FastPolicy3, NW, C>(t);
+      if (t.alg == 2) return pick_fast_tuned<gpp::FastPolicyT<2, 3>, NW, C>(t);
       if (t.alg == 1 && t.sq == 1) return pick_fast_tuned<gpp::FastPolicyT<1, 1>, NW, C>(t);
       if (t.alg == 1 && t.sq == 2) return pick_fast_tuned<gpp::FastPolicyT<1, 2>, NW, C>(t);
       if (t.alg == 1) return pick_fast_tuned<gpp::FastPolicyT<1, 3>, NW, C>(t);
@@ -257,6 +261,7 @@ int make_plan(gpp_ctx* c, int variant, int nw_group, bool count, Plan* pl) {
   GPP_CUDA(cudaFuncGetAttributes(&attr, fn));
   pl->regs = attr.numRegs;
   pl->blocks_per_sm = std::max(bps, 1);
+  if (tune.bps > 0) pl->blocks_per_sm = std::min(pl->blocks_per_sm, tune.bps);
   const long long slots = static_cast<long long>(pl->blocks_per_sm) * c->num_sms;
   // Band chunk: as long as possible (amortises the per-item state load) while
   // leaving >= 32 items per resident CTA so the static round-robin balances.
@@ -306,6 +311,7 @@ int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool
     p.n_igptile = pl.n_igptile;
     p.bchunk = pl.bchunk;
     p.n_items = pl.n_items;
+    p.wxmax = c->wxmax;
     p.partials = c->partials.ptr;
     p.cpartials = c->cpartials.ptr;
     KernelFn fn = pick_kernel(variant, nwg, pl.igp_t, count);
@@ -446,6 +452,8 @@ int gpp_upload(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32
     for (int64_t b = 0; b < nb; ++b)
       std::memcpy(c->h_wx + static_cast<size_t>(b) * nw, wx, nw * sizeof(double));
   }
+  double wxmax = 0.0;
+  for (size_t k = 0; k < n_wx; ++k) wxmax = std::max(wxmax, std::fabs(c->h_wx[k]));
   cudaStream_t s = c->stream;
   GPP_CUDA(cudaMemcpyAsync(c->wtilde.ptr, wtilde, n_wt * sizeof(double2), cudaMemcpyHostToDevice, s));
   GPP_CUDA(cudaMemcpyAsync(c->eps.ptr, i_eps, n_wt * sizeof(double2), cudaMemcpyHostToDevice, s));
@@ -459,6 +467,7 @@ int gpp_upload(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32
   c->ngpown = ngpown;
   c->ncouls = ncouls;
   c->nw = nw;
+  c->wxmax = wxmax;
   c->have_problem = true;
   return GPP_OK;
 }
