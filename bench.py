@@ -343,13 +343,13 @@ def run_ours(args, dist: Dist):
             d2h = 8 * 4 * args.nw + 16
             for _ in range(2):
                 ctx.upload(p, (b0, b1), force=True)
-                ctx.run(args.variant)
+                ctx.run(args.variant, counts=False)
             dist.barrier()
             dist.sync()
             t0 = time.perf_counter()
             for _ in range(args.e2e_steps):
                 ctx.upload(p, (b0, b1), force=True)
-                ctx.run(args.variant)
+                ctx.run(args.variant, counts=False)
             dist.sync()
             el = time.perf_counter() - t0
             dist.barrier()

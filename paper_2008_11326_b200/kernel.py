@@ -119,8 +119,13 @@ class GPPContext:
         self._key = key if cacheable else None
         self._keep = arrays if cacheable else None  # pin ids while cached
 
-    def run(self, variant: str = "rcp_sq"):
-        """Evaluate the uploaded problem: (GPPResult, (near, far), kernel_ms)."""
+    def run(self, variant: str = "rcp_sq", counts: bool = True):
+        """Evaluate the uploaded problem: (GPPResult, (near, far) | None, kernel_ms).
+
+        ``counts=True`` runs the counting kernel (branch statistics as a
+        by-product, two predicated integer adds per instance); ``False`` runs
+        the production kernel that evaluate_variant uses.
+        """
         code = _variant_code(variant)
         if self.nw < 1:
             raise DomainError("no problem uploaded")
@@ -128,14 +133,14 @@ class GPPContext:
         asx = np.empty(2 * self.nw, dtype=np.float64)
         nf = np.zeros(2, dtype=np.int64)
         ms = ctypes.c_float()
+        nf_ptr = nf.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)) if counts else None
         _lib.check(
-            self._lib.gpp_run(self._h, code, _lib.dptr(ach), _lib.dptr(asx),
-                              nf.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ctypes.byref(ms)),
+            self._lib.gpp_run(self._h, code, _lib.dptr(ach), _lib.dptr(asx), nf_ptr, ctypes.byref(ms)),
             "gpp_run",
         )
         result = GPPResult(achtemp=ach.view(np.complex128).copy(),
                            asxtemp=asx.view(np.complex128).copy())
-        return result, (int(nf[0]), int(nf[1])), float(ms.value)
+        return result, ((int(nf[0]), int(nf[1])) if counts else None), float(ms.value)
 
     def time(self, variant: str = "rcp_sq", iters: int = 10) -> tuple[float, float]:
         """Device-resident timing of ``iters`` evaluations: (total_ms, main_kernel_ms)."""
@@ -176,20 +181,22 @@ def get_context(device: int = 0) -> GPPContext:
     return ctx
 
 
-def evaluate(problem, variant: str = "rcp_sq", device: int = 0):
-    """Upload (cached) + run: (GPPResult, BranchStats, kernel_ms)."""
+def evaluate(problem, variant: str = "rcp_sq", device: int = 0, counts: bool = True):
+    """Upload (cached) + run: (GPPResult, BranchStats | None, kernel_ms)."""
     ctx = get_context(device)
     ctx.upload(problem)
-    result, (near, far), ms = ctx.run(variant)
-    nb, ng, nc = ctx.dims
-    stats = BranchStats(instances=ctx.nw * nb * ng * nc, near=near, far=far)
+    result, nf, ms = ctx.run(variant, counts=counts)
+    stats = None
+    if nf is not None:
+        nb, ng, nc = ctx.dims
+        stats = BranchStats(instances=ctx.nw * nb * ng * nc, near=nf[0], far=nf[1])
     return result, stats, ms
 
 
 def evaluate_variant(problem, variant: str, device: int = 0) -> GPPResult:
     """Drop-in for rooflab.gpp.kernel.evaluate_variant (kernel.py:98-114)."""
     _variant_code(variant)
-    return evaluate(problem, variant, device)[0]
+    return evaluate(problem, variant, device, counts=False)[0]
 
 
 def branch_stats(problem, variant: str, device: int = 0) -> BranchStats:
@@ -201,7 +208,7 @@ def branch_stats(problem, variant: str, device: int = 0) -> BranchStats:
 def reference_result(problem, device: int = 0) -> GPPResult:
     """The literal-nest formulation (problem.py:179-208: library complex
     division and magnitude predicates) evaluated per instance on the GPU."""
-    return evaluate(problem, "div", device)[0]
+    return evaluate(problem, "div", device, counts=False)[0]
 
 
 def fp64_peak(device: int = 0, iters: int = 200_000) -> tuple[float, float]:

@@ -45,10 +45,14 @@ def _ids(cases):
 @pytest.mark.parametrize("case", SMALL, ids=_ids(SMALL))
 @pytest.mark.parametrize("variant", ["div", "rcp", "rcp_sq"])
 def test_small_cases_vs_reference(case, variant):
+    """Both kernels: the counting one (general path) and the production one
+    evaluate_variant runs (regular-item fast path)."""
     p = synth_problem(*case["dims"], seed=case["seed"], nw=case["nw"])
     got, stats, _ = evaluate(p, variant)
-    assert max_rel_error(got, _R(case["reference_result"])) <= TOL
-    assert max_rel_error(got, _R(case["evaluate_variant"][variant])) <= TOL
+    fast = evaluate_variant(p, variant)
+    for r in (got, fast):
+        assert max_rel_error(r, _R(case["reference_result"])) <= TOL
+        assert max_rel_error(r, _R(case["evaluate_variant"][variant])) <= TOL
     assert [stats.instances, stats.near, stats.far] == case["branch_stats"][variant]
 
 
@@ -57,9 +61,11 @@ def test_big_cases_vs_reference(case):
     nb, ng, nc = case["dims"]
     p = synth_problem(nb, ng, nc, seed=case["seed"], nw=case["nw"], check=nb * ng * nc < 10**10)
     got, stats, _ = evaluate(p, "rcp_sq")
+    fast = evaluate_variant(p, "rcp_sq")
     want = _R(case.get("reference_result") or case["evaluate_variant"]["rcp_sq"])
-    err = max_rel_error(got, want)
-    assert err <= TOL, err
+    for r in (got, fast):
+        err = max_rel_error(r, want)
+        assert err <= TOL, err
     assert [stats.instances, stats.near, stats.far] == case["branch_stats"]["rcp_sq"]
 
 
@@ -92,6 +98,7 @@ def test_other_frequency_counts_vs_oracle(nw):
     for variant in ("rcp_sq", "div"):
         got, stats, _ = evaluate(p, variant)
         assert max_rel_error(got, want) <= TOL
+        assert max_rel_error(evaluate_variant(p, variant), want) <= TOL
         assert (stats.instances, stats.near, stats.far) == (inst, near, far)
 
 
@@ -106,6 +113,7 @@ def test_band_indexed_wx_vs_oracle():
     for variant in ("rcp_sq", "rcp", "div"):
         got, stats, _ = evaluate(p, variant)
         assert max_rel_error(got, want) <= TOL, variant
+        assert max_rel_error(evaluate_variant(p, variant), want) <= TOL, variant
         assert (stats.instances, stats.near, stats.far) == (inst, near, far), variant
 
 
@@ -173,4 +181,24 @@ def test_degenerate_inputs():
     for variant in ("rcp_sq", "div", "rcp"):
         got, stats, _ = evaluate(q, variant)
         assert max_rel_error(got, want) <= TOL, variant
+        assert max_rel_error(evaluate_variant(q, variant), want) <= TOL, variant
         assert (stats.near, stats.far) == (near, far), variant
+
+
+def test_irregular_items_take_the_general_path():
+    """Items with a degenerate-capable (ig, igp) -- wt.im == 0 makes d = 0
+    possible, tiny |wt| makes |delw| <= 1e-12 possible -- must reproduce the
+    reference's degenerate handling in the production kernel too."""
+    p = synth_problem(12, 5, 300, seed=7)
+    wt = np.array(p.wtilde, order="F")
+    wt[3, 1] = complex(p.wx[0], 0.0)    # wdiff == 0 exactly for iw 0 (real wtilde)
+    wt[10, 2] = 1e-14 + 0j              # |delw| ~ 1e-14: degenerate
+    wt[200, 4] = complex(0.3, 0.0)      # real wtilde, not singular
+    q = GPPProblem(12, 5, 300, wt, p.i_eps, p.aqsntemp, p.aqsmtemp, p.wx)
+    want = orc.evaluate_variant(q, "rcp_sq")
+    inst, near, far = orc.branch_stats(q, "rcp_sq")
+    got, stats, _ = evaluate(q, "rcp_sq")
+    assert (stats.near, stats.far) == (near, far)
+    for r in (got, evaluate_variant(q, "rcp_sq")):
+        assert np.all(np.isfinite(r.achtemp)) and np.all(np.isfinite(r.asxtemp))
+        assert max_rel_error(r, want) <= TOL
