@@ -97,23 +97,9 @@ class Dist:
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
 
-    def bcast_bytes(self, payload: bytes | None) -> bytes:
-        if not self.pg:
-            return payload
-        obj = [payload]
-        self.pg.broadcast_object_list(obj, src=0)
-        return obj[0]
-
     def close(self):
         if self.pg:
             self.pg.destroy_process_group()
-
-
-def band_range(nbands: int, world: int, rank: int) -> tuple[int, int]:
-    """Contiguous, balanced band shard [b0, b1) of rank."""
-    base, extra = divmod(nbands, world)
-    b0 = rank * base + min(rank, extra)
-    return b0, b0 + base + (1 if rank < extra else 0)
 
 
 # ----------------------------------------------------------------------------
@@ -287,7 +273,7 @@ def _config(args, dims):
 
 
 def run_ours(args, dist: Dist):
-    from paper_2008_11326_b200 import GPPContext, comm_unique_id, fp64_peak, synth_problem
+    from paper_2008_11326_b200 import fp64_peak, synth_problem
     from paper_2008_11326_b200._lib import load
     from paper_2008_11326_b200.counters import algorithmic_flops
 
@@ -295,17 +281,16 @@ def run_ours(args, dist: Dist):
     nb, ng, nc = dims
     device = dist.local_rank
     p = synth_problem(nb, ng, nc, seed=args.seed, nw=args.nw, check=False)
-    b0, b1 = band_range(nb, dist.world, dist.rank)
-
     load()
     # FP64 roofline denominator: measured live on this device (MEASURED_PEAKS.json has no FP64).
     fp64_peak(device, 20_000)
     peak_tf, _ = fp64_peak(device, 300_000)
 
-    ctx = GPPContext(device)
-    if dist.world > 1:
-        uid = dist.bcast_bytes(comm_unique_id() if dist.rank == 0 else None)
-        ctx.comm_init(dist.world, dist.rank, uid)
+    from paper_2008_11326_b200.dist import ShardedGPP
+
+    shard = ShardedGPP.from_torch(device) if dist.world > 1 else ShardedGPP(device, 0, 1, None)
+    ctx = shard.ctx
+    b0, b1 = shard.band_range(nb)
     ctx.upload(p, (b0, b1))
     result, (near, far), _ = ctx.run(args.variant)  # combined over ranks
     info = ctx.kernel_info(args.variant)

@@ -1,0 +1,86 @@
+"""Band (n1) sharding across GPUs: one process per GPU.
+
+SURVEY.md section 8e: the band sum is an independent reduction, so rank r
+evaluates the contiguous band range [b0, b1) (its columns of aqsntemp and
+aqsmtemp are one contiguous slice each in F-order), wtilde / i_eps / wx are
+replicated, and the per-rank partial achtemp / asxtemp and branch counts
+(4*nw doubles + 2 integers) are combined by ONE ncclAllReduce issued by the
+library on its own stream right after the finalize kernel (gpp_run /
+gpp_time, csrc/gpp_lib.cu).  torch.distributed is only the bootstrap that
+broadcasts the 128-byte NCCL unique id.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .kernel import GPPContext, comm_unique_id
+from .problem import GPPProblem
+
+
+def band_range(nbands: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced band shard [b0, b1) of ``rank`` (first ranks take
+    the remainder)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world of {world}")
+    base, extra = divmod(int(nbands), world)
+    b0 = rank * base + min(rank, extra)
+    return b0, b0 + base + (1 if rank < extra else 0)
+
+
+def shard_problem(problem, b0: int, b1: int) -> GPPProblem:
+    """The band shard [b0, b1) of a problem as its own GPPProblem (views).
+
+    Used by the CPU tests to check the partition against the oracle; the GPU
+    path passes the whole arrays plus the range to gpp_upload instead.
+    """
+    wx = np.asarray(problem.wx)
+    if wx.ndim == 2:
+        wx = wx[:, b0:b1]
+    return GPPProblem(
+        nbands=b1 - b0,
+        ngpown=problem.ngpown,
+        ncouls=problem.ncouls,
+        wtilde=problem.wtilde,
+        i_eps=problem.i_eps,
+        aqsntemp=problem.aqsntemp[:, b0:b1],
+        aqsmtemp=problem.aqsmtemp[:, b0:b1],
+        wx=wx,
+        seed=getattr(problem, "seed", None),
+    )
+
+
+class ShardedGPP:
+    """One rank of a band-sharded evaluation (its GPU context + NCCL comm)."""
+
+    def __init__(self, device: int, rank: int, world: int, unique_id: bytes | None):
+        self.rank, self.world = int(rank), int(world)
+        self.ctx = GPPContext(device)
+        if self.world > 1:
+            if unique_id is None:
+                raise ValueError("a NCCL unique id is required for world > 1")
+            self.ctx.comm_init(self.world, self.rank, unique_id)
+
+    @classmethod
+    def from_torch(cls, device: int) -> "ShardedGPP":
+        """Bootstrap from an initialised torch.distributed process group."""
+        import torch.distributed as tdist
+
+        world, rank = tdist.get_world_size(), tdist.get_rank()
+        obj = [comm_unique_id() if rank == 0 else None]
+        if world > 1:
+            tdist.broadcast_object_list(obj, src=0)
+        return cls(device, rank, world, obj[0])
+
+    def band_range(self, nbands: int) -> tuple[int, int]:
+        return band_range(nbands, self.world, self.rank)
+
+    def upload(self, problem, force: bool = False) -> None:
+        self.ctx.upload(problem, self.band_range(int(problem.nbands)), force=force)
+
+    def run(self, variant: str = "rcp_sq", counts: bool = True):
+        """Evaluate this rank's shard; the result is the all-rank total."""
+        return self.ctx.run(variant, counts=counts)
+
+    def close(self) -> None:
+        self.ctx.close()
