@@ -327,14 +327,12 @@ def run_ours(args, dist: Dist):
                    + 8 * args.nw * (b1 - b0))
             d2h = 8 * 4 * args.nw + 16
             for _ in range(2):
-                ctx.upload(p, (b0, b1), force=True)
-                ctx.run(args.variant, counts=False)
+                ctx.evaluate_host(p, args.variant, band_range=(b0, b1))
             dist.barrier()
             dist.sync()
             t0 = time.perf_counter()
             for _ in range(args.e2e_steps):
-                ctx.upload(p, (b0, b1), force=True)
-                ctx.run(args.variant, counts=False)
+                ctx.evaluate_host(p, args.variant, band_range=(b0, b1))
             dist.sync()
             el = time.perf_counter() - t0
             dist.barrier()
@@ -342,7 +340,7 @@ def run_ours(args, dist: Dist):
             e2e = {"value": flops_job / (el / args.e2e_steps) / 1e12, "unit": "TFLOP/s",
                    "ms_per_step": el / args.e2e_steps * 1e3, "steps": args.e2e_steps,
                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                   "path": "GPPContext.upload(force) + GPPContext.run -> gpp_upload + gpp_run (C ABI)"}
+                   "path": "GPPContext.evaluate_host -> gpp_evaluate_host (C ABI): ig-slab H2D pipelined with the kernel, result D2H"}
         finally:
             for a in arrays:
                 lib.gpp_host_unregister(a.ctypes.data)

@@ -102,6 +102,22 @@ int gpp_upload(gpp_ctx* ctx, int64_t nbands, int64_t ngpown, int64_t ncouls, int
 int gpp_run(gpp_ctx* ctx, int32_t variant, double* achtemp, double* asxtemp,
             int64_t* near_far, float* kernel_ms);
 
+/* Upload + evaluate in one call, with the host->device copy pipelined
+ * against the computation: the ig rows of wtilde / i_eps / aqsntemp are
+ * copied in `slabs` ig slabs (<= 0: 16) on a copy stream, and the kernel for
+ * slab s starts as soon as its rows have landed, while slab s+1 is in
+ * flight.  Arguments as gpp_upload + gpp_run; `ms` (nullable) receives the
+ * device time from the first copy to the end of the computation.  Host
+ * arrays should be page-locked (gpp_host_register) for the copies to be
+ * asynchronous.  Afterwards the problem is resident, as after gpp_upload.
+ * This is the end-to-end path of evaluate_variant on a problem that is not
+ * yet on the device (kernel.py:98-114). */
+int gpp_evaluate_host(gpp_ctx* ctx, int32_t variant, int64_t nbands, int64_t ngpown,
+                      int64_t ncouls, int32_t nw, const double* wtilde, const double* i_eps,
+                      const double* aqsntemp, const double* aqsmtemp, const double* wx,
+                      int32_t wx_band_indexed, int64_t band0, int64_t band1, int32_t slabs,
+                      double* achtemp, double* asxtemp, int64_t* near_far, float* ms);
+
 /* Device-resident timing: `iters` back-to-back evaluations on the context's
  * stream (compute kernels + finalize + allreduce when attached, no host
  * copies).  total_ms = event time of the whole run; main_ms = summed event

@@ -47,6 +47,7 @@ struct Params {
   const double* wxb;       // (nb, nw_total): wxb[band * nw_total + iw]
   int ncouls, ngpown, nbands;
   int nw_total, iw0;       // this launch evaluates iw in [iw0, iw0 + NW)
+  int igblk0;              // first 256-ig block of this launch (ig slab)
   int n_igblk, n_igptile, bchunk;
   long long n_items;
   double wxmax;            // max |wx| over the uploaded bands (regular-item guard)
@@ -580,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, MINB) gpp_main_kernel(const Params p
     const long long rest = item / p.n_igptile;
     const int igb = static_cast<int>(rest % p.n_igblk);
     const int bc = static_cast<int>(rest / p.n_igblk);
-    const int ig = igb * kThreads + tid;
+    const int ig = (p.igblk0 + igb) * kThreads + tid;
     const bool vig = ig < p.ncouls;
     const int igc = vig ? ig : p.ncouls - 1;
     const int b0 = bc * p.bchunk;

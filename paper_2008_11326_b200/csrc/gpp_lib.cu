@@ -86,7 +86,9 @@ struct gpp_ctx {
   int device = -1;
   bool initialized = false;
   cudaStream_t stream = nullptr;
+  cudaStream_t cstream = nullptr;  // H2D copies of the pipelined evaluate
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> slab_ev;
   int num_sms = 0;
 
   // Problem (local band shard).
@@ -124,6 +126,7 @@ int ensure_init(gpp_ctx* c) {
   DeviceGuard g(c->device);
   if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
   GPP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  GPP_CUDA(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
   for (auto& ev : c->ev) GPP_CUDA(cudaEventCreate(&ev));
   GPP_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
   c->initialized = true;
@@ -285,41 +288,65 @@ int nw_groups(int nw, std::vector<std::pair<int, int>>* groups) {
 
 // Enqueue one full evaluation on c->stream.  If ev_main is non-null, the
 // main kernels of all frequency groups are bracketed by ev_main[0..1].
-int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool allreduce) {
+// Optional ig-slab schedule of one evaluation: slab s covers the 256-ig blocks
+// [blk0[s], blk0[s+1]) and its launch waits on ready[s] (the H2D of its rows).
+struct SlabSched {
+  std::vector<int> blk0;             // size S + 1
+  std::vector<cudaEvent_t> ready;    // size S (may be empty: no waits)
+};
+
+// Enqueue one full evaluation on c->stream.  If ev_main is non-null, the
+// main kernels of all frequency groups are bracketed by ev_main[0..1].
+int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool allreduce,
+                 const SlabSched* sched = nullptr) {
   std::vector<std::pair<int, int>> groups;
   nw_groups(c->nw, &groups);
+  const int n_blk_all = static_cast<int>((c->ncouls + gpp::kThreads - 1) / gpp::kThreads);
+  SlabSched whole;
+  whole.blk0 = {0, n_blk_all};
+  const SlabSched& sl = sched ? *sched : whole;
+  const int n_slabs = static_cast<int>(sl.blk0.size()) - 1;
   bool first = true;
   for (size_t gi = 0; gi < groups.size(); ++gi) {
     const int iw0 = groups[gi].first, nwg = groups[gi].second;
     Plan pl;
     int rc = make_plan(c, variant, nwg, count, &pl);
     if (rc) return rc;
-    GPP_CUDA(c->partials.ensure(static_cast<size_t>(pl.grid) * 4 * gpp::kMaxNwGroup));
-    GPP_CUDA(c->cpartials.ensure(static_cast<size_t>(pl.grid) * 2));
-    gpp::Params p;
-    p.wtilde = c->wtilde.ptr;
-    p.eps = c->eps.ptr;
-    p.aqsn = c->aqsn.ptr;
-    p.aqsm = c->aqsm.ptr;
-    p.wxb = c->wxb.ptr;
-    p.ncouls = static_cast<int>(c->ncouls);
-    p.ngpown = static_cast<int>(c->ngpown);
-    p.nbands = static_cast<int>(c->nbands);
-    p.nw_total = c->nw;
-    p.iw0 = iw0;
-    p.n_igblk = pl.n_igblk;
-    p.n_igptile = pl.n_igptile;
-    p.bchunk = pl.bchunk;
-    p.n_items = pl.n_items;
-    p.wxmax = c->wxmax;
-    p.partials = c->partials.ptr;
-    p.cpartials = c->cpartials.ptr;
+    GPP_CUDA(c->partials.ensure(static_cast<size_t>(pl.grid) * n_slabs * 4 * gpp::kMaxNwGroup));
+    GPP_CUDA(c->cpartials.ensure(static_cast<size_t>(pl.grid) * n_slabs * 2));
     KernelFn fn = pick_kernel(variant, nwg, pl.igp_t, count);
+    int rows = 0;  // partial rows written by this frequency group
     if (ev_main && gi == 0) GPP_CUDA(cudaEventRecord(ev_main[0], c->stream));
-    fn<<<pl.grid, gpp::kThreads, 0, c->stream>>>(p);
-    GPP_CUDA(cudaGetLastError());
+    for (int s = 0; s < n_slabs; ++s) {
+      const int nblk = sl.blk0[s + 1] - sl.blk0[s];
+      if (nblk <= 0) continue;
+      if (gi == 0 && !sl.ready.empty()) GPP_CUDA(cudaStreamWaitEvent(c->stream, sl.ready[s], 0));
+      gpp::Params p;
+      p.wtilde = c->wtilde.ptr;
+      p.eps = c->eps.ptr;
+      p.aqsn = c->aqsn.ptr;
+      p.aqsm = c->aqsm.ptr;
+      p.wxb = c->wxb.ptr;
+      p.ncouls = static_cast<int>(c->ncouls);
+      p.ngpown = static_cast<int>(c->ngpown);
+      p.nbands = static_cast<int>(c->nbands);
+      p.nw_total = c->nw;
+      p.iw0 = iw0;
+      p.igblk0 = sl.blk0[s];
+      p.n_igblk = nblk;
+      p.n_igptile = pl.n_igptile;
+      p.bchunk = pl.bchunk;
+      p.n_items = pl.n_items / pl.n_igblk * nblk;
+      p.wxmax = c->wxmax;
+      const int grid = static_cast<int>(std::min<long long>(pl.grid, p.n_items));
+      p.partials = c->partials.ptr + static_cast<size_t>(rows) * 4 * nwg;
+      p.cpartials = c->cpartials.ptr + static_cast<size_t>(rows) * 2;
+      fn<<<grid, gpp::kThreads, 0, c->stream>>>(p);
+      GPP_CUDA(cudaGetLastError());
+      rows += grid;
+    }
     if (ev_main && gi + 1 == groups.size()) GPP_CUDA(cudaEventRecord(ev_main[1], c->stream));
-    pick_finalize(nwg)<<<1, 256, 0, c->stream>>>(c->partials.ptr, c->cpartials.ptr, pl.grid,
+    pick_finalize(nwg)<<<1, 256, 0, c->stream>>>(c->partials.ptr, c->cpartials.ptr, rows,
                                                   c->nw, iw0, variant == GPP_VARIANT_RCP_SQ,
                                                   first ? 1 : 0, count ? 1 : 0, c->out.ptr,
                                                   c->counts.ptr);
@@ -375,6 +402,7 @@ void gpp_destroy(gpp_ctx* c) {
   if (c->initialized) {
     DeviceGuard g(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->cstream) cudaStreamSynchronize(c->cstream);
     if (c->comm) ncclCommDestroy(c->comm);
     c->wtilde.release();
     c->eps.release();
@@ -390,52 +418,64 @@ void gpp_destroy(gpp_ctx* c) {
     if (c->h_wx) cudaFreeHost(c->h_wx);
     for (auto& ev : c->ev)
       if (ev) cudaEventDestroy(ev);
+    for (auto& ev : c->slab_ev) cudaEventDestroy(ev);
+    if (c->cstream) cudaStreamDestroy(c->cstream);
     if (c->stream) cudaStreamDestroy(c->stream);
   }
   delete c;
 }
 
-int gpp_upload(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw,
-               const double* wtilde, const double* i_eps, const double* aqsntemp,
-               const double* aqsmtemp, const double* wx, int32_t wx_band_indexed,
-               int64_t band0, int64_t band1) {
-  if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
-  if (nbands < 1 || ngpown < 1 || ncouls < 1)
-    return fail(GPP_ERR_ARG, "nbands, ngpown and ncouls must all be at least 1");
-  if (nw < 1) return fail(GPP_ERR_ARG, "nw must be at least 1");
-  if (!wtilde || !i_eps || !aqsntemp || !aqsmtemp || !wx)
-    return fail(GPP_ERR_ARG, "input array pointer is NULL");
-  if (band0 < 0 || band1 > nbands || band0 >= band1)
-    return fail(GPP_ERR_ARG, "band range [" + std::to_string(band0) + ", " +
-                                 std::to_string(band1) + ") is empty or outside [0, " +
-                                 std::to_string(nbands) + ")");
-  const int64_t kIntMax = 0x7fffffff;
-  if (ncouls > kIntMax || ngpown > kIntMax || nbands > kIntMax ||
-      (ncouls + gpp::kThreads) * (ngpown + gpp::kMaxIgpTile) > (int64_t{1} << 40))
-    return fail(GPP_ERR_ARG, "problem dimensions exceed the supported range");
-  int rc = ensure_init(c);
-  if (rc) return rc;
-  DeviceGuard g(c->device);
-  if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+}  // extern "C"
 
-  const int64_t nb = band1 - band0;
-  const size_t n_wt = static_cast<size_t>(ncouls) * ngpown;
-  const size_t n_an = static_cast<size_t>(ncouls) * nb;
-  const size_t n_am = static_cast<size_t>(ngpown) * nb;
-  const size_t n_wx = static_cast<size_t>(nb) * nw;
+namespace {
+
+struct HostProblem {
+  int64_t nbands, ngpown, ncouls;
+  int32_t nw;
+  const double *wtilde, *i_eps, *aqsntemp, *aqsmtemp, *wx;
+  int32_t wx_band_indexed;
+  int64_t band0, band1;
+};
+
+int validate(const gpp_ctx* c, const HostProblem& h) {
+  if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
+  if (h.nbands < 1 || h.ngpown < 1 || h.ncouls < 1)
+    return fail(GPP_ERR_ARG, "nbands, ngpown and ncouls must all be at least 1");
+  if (h.nw < 1) return fail(GPP_ERR_ARG, "nw must be at least 1");
+  if (!h.wtilde || !h.i_eps || !h.aqsntemp || !h.aqsmtemp || !h.wx)
+    return fail(GPP_ERR_ARG, "input array pointer is NULL");
+  if (h.band0 < 0 || h.band1 > h.nbands || h.band0 >= h.band1)
+    return fail(GPP_ERR_ARG, "band range [" + std::to_string(h.band0) + ", " +
+                                 std::to_string(h.band1) + ") is empty or outside [0, " +
+                                 std::to_string(h.nbands) + ")");
+  const int64_t kIntMax = 0x7fffffff;
+  if (h.ncouls > kIntMax || h.ngpown > kIntMax || h.nbands > kIntMax ||
+      (h.ncouls + gpp::kThreads) * (h.ngpown + gpp::kMaxIgpTile) > (int64_t{1} << 40))
+    return fail(GPP_ERR_ARG, "problem dimensions exceed the supported range");
+  return GPP_OK;
+}
+
+// Size the device buffers and the pinned staging for a problem shard, and
+// expand wx to the band-indexed layout on the host (pinned).  No copies yet.
+int prepare(gpp_ctx* c, const HostProblem& h) {
+  const int64_t nb = h.band1 - h.band0;
+  const size_t n_wt = static_cast<size_t>(h.ncouls) * h.ngpown;
+  const size_t n_an = static_cast<size_t>(h.ncouls) * nb;
+  const size_t n_am = static_cast<size_t>(h.ngpown) * nb;
+  const size_t n_wx = static_cast<size_t>(nb) * h.nw;
   GPP_CUDA(c->wtilde.ensure(n_wt));
   GPP_CUDA(c->eps.ensure(n_wt));
   GPP_CUDA(c->aqsn.ensure(n_an));
   GPP_CUDA(c->aqsm.ensure(n_am));
   GPP_CUDA(c->wxb.ensure(n_wx));
-  GPP_CUDA(c->out.ensure(4 * static_cast<size_t>(nw)));
+  GPP_CUDA(c->out.ensure(4 * static_cast<size_t>(h.nw)));
   GPP_CUDA(c->counts.ensure(2));
-  if (c->h_out_cap < 4 * static_cast<size_t>(nw)) {
+  if (c->h_out_cap < 4 * static_cast<size_t>(h.nw)) {
     if (c->h_out) cudaFreeHost(c->h_out);
     c->h_out = nullptr;
     c->h_out_cap = 0;
-    GPP_CUDA(cudaMallocHost(&c->h_out, 4 * sizeof(double) * nw));
-    c->h_out_cap = 4 * static_cast<size_t>(nw);
+    GPP_CUDA(cudaMallocHost(&c->h_out, 4 * sizeof(double) * h.nw));
+    c->h_out_cap = 4 * static_cast<size_t>(h.nw);
   }
   if (!c->h_counts) GPP_CUDA(cudaMallocHost(&c->h_counts, 2 * sizeof(unsigned long long)));
   if (c->h_wx_cap < n_wx) {
@@ -445,46 +485,52 @@ int gpp_upload(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32
     GPP_CUDA(cudaMallocHost(&c->h_wx, n_wx * sizeof(double)));
     c->h_wx_cap = n_wx;
   }
-  // wx -> band-indexed [band][iw] for the shard.
-  if (wx_band_indexed) {
-    std::memcpy(c->h_wx, wx + static_cast<size_t>(band0) * nw, n_wx * sizeof(double));
+  // The device stream must be done with the staging before it is rewritten.
+  GPP_CUDA(cudaStreamSynchronize(c->cstream));
+  if (h.wx_band_indexed) {
+    std::memcpy(c->h_wx, h.wx + static_cast<size_t>(h.band0) * h.nw, n_wx * sizeof(double));
   } else {
     for (int64_t b = 0; b < nb; ++b)
-      std::memcpy(c->h_wx + static_cast<size_t>(b) * nw, wx, nw * sizeof(double));
+      std::memcpy(c->h_wx + static_cast<size_t>(b) * h.nw, h.wx, h.nw * sizeof(double));
   }
   double wxmax = 0.0;
   for (size_t k = 0; k < n_wx; ++k) wxmax = std::max(wxmax, std::fabs(c->h_wx[k]));
-  cudaStream_t s = c->stream;
-  GPP_CUDA(cudaMemcpyAsync(c->wtilde.ptr, wtilde, n_wt * sizeof(double2), cudaMemcpyHostToDevice, s));
-  GPP_CUDA(cudaMemcpyAsync(c->eps.ptr, i_eps, n_wt * sizeof(double2), cudaMemcpyHostToDevice, s));
-  GPP_CUDA(cudaMemcpyAsync(c->aqsn.ptr, aqsntemp + 2 * static_cast<size_t>(band0) * ncouls,
-                           n_an * sizeof(double2), cudaMemcpyHostToDevice, s));
-  GPP_CUDA(cudaMemcpyAsync(c->aqsm.ptr, aqsmtemp + 2 * static_cast<size_t>(band0) * ngpown,
-                           n_am * sizeof(double2), cudaMemcpyHostToDevice, s));
-  GPP_CUDA(cudaMemcpyAsync(c->wxb.ptr, c->h_wx, n_wx * sizeof(double), cudaMemcpyHostToDevice, s));
-  GPP_CUDA(cudaStreamSynchronize(s));
   c->nbands = nb;
-  c->ngpown = ngpown;
-  c->ncouls = ncouls;
-  c->nw = nw;
+  c->ngpown = h.ngpown;
+  c->ncouls = h.ncouls;
+  c->nw = h.nw;
   c->wxmax = wxmax;
-  c->have_problem = true;
   return GPP_OK;
 }
 
-int gpp_run(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp, int64_t* near_far,
-            float* kernel_ms) {
-  if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
-  int rc = check_variant(variant);
-  if (rc) return rc;
-  if (!achtemp || !asxtemp) return fail(GPP_ERR_ARG, "output pointer is NULL");
-  if (!c->have_problem) return fail(GPP_ERR_ARG, "no problem uploaded");
-  DeviceGuard g(c->device);
-  if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
-  GPP_CUDA(cudaEventRecord(c->ev[2], c->stream));
-  rc = enqueue_eval(c, variant, near_far != nullptr, nullptr, false);
-  if (rc) return rc;
-  GPP_CUDA(cudaEventRecord(c->ev[3], c->stream));
+// H2D of the small arrays (aqsmtemp shard, expanded wx) on stream s.
+int copy_small(gpp_ctx* c, const HostProblem& h, cudaStream_t s) {
+  const int64_t nb = h.band1 - h.band0;
+  GPP_CUDA(cudaMemcpyAsync(c->aqsm.ptr, h.aqsmtemp + 2 * static_cast<size_t>(h.band0) * h.ngpown,
+                           static_cast<size_t>(h.ngpown) * nb * sizeof(double2),
+                           cudaMemcpyHostToDevice, s));
+  GPP_CUDA(cudaMemcpyAsync(c->wxb.ptr, c->h_wx, static_cast<size_t>(nb) * h.nw * sizeof(double),
+                           cudaMemcpyHostToDevice, s));
+  return GPP_OK;
+}
+
+// H2D of the ig rows [i0, i1) of wtilde, i_eps and the aqsntemp shard:
+// strided (2D) copies of the F-order arrays, one row segment per column.
+int copy_rows(gpp_ctx* c, const HostProblem& h, int64_t i0, int64_t i1, cudaStream_t s) {
+  const size_t pitch = static_cast<size_t>(h.ncouls) * sizeof(double2);
+  const size_t width = static_cast<size_t>(i1 - i0) * sizeof(double2);
+  const size_t off = static_cast<size_t>(i0);
+  GPP_CUDA(cudaMemcpy2DAsync(c->wtilde.ptr + off, pitch, h.wtilde + 2 * off, pitch, width,
+                             h.ngpown, cudaMemcpyHostToDevice, s));
+  GPP_CUDA(cudaMemcpy2DAsync(c->eps.ptr + off, pitch, h.i_eps + 2 * off, pitch, width, h.ngpown,
+                             cudaMemcpyHostToDevice, s));
+  GPP_CUDA(cudaMemcpy2DAsync(c->aqsn.ptr + off, pitch,
+                             h.aqsntemp + 2 * (static_cast<size_t>(h.band0) * h.ncouls + off),
+                             pitch, width, h.band1 - h.band0, cudaMemcpyHostToDevice, s));
+  return GPP_OK;
+}
+
+int finish_run(gpp_ctx* c, double* achtemp, double* asxtemp, int64_t* near_far) {
   if (c->comm && c->nranks > 1) {
     GPP_NCCL(ncclGroupStart());
     GPP_NCCL(ncclAllReduce(c->out.ptr, c->out.ptr, 4 * c->nw, ncclDouble, ncclSum, c->comm,
@@ -504,6 +550,107 @@ int gpp_run(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp, int64
     near_far[0] = static_cast<int64_t>(c->h_counts[0]);
     near_far[1] = static_cast<int64_t>(c->h_counts[1]);
   }
+  return GPP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gpp_upload(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw,
+               const double* wtilde, const double* i_eps, const double* aqsntemp,
+               const double* aqsmtemp, const double* wx, int32_t wx_band_indexed,
+               int64_t band0, int64_t band1) {
+  const HostProblem h{nbands, ngpown, ncouls, nw, wtilde, i_eps, aqsntemp, aqsmtemp, wx,
+                      wx_band_indexed, band0, band1};
+  int rc = validate(c, h);
+  if (rc) return rc;
+  rc = ensure_init(c);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
+  if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+  c->have_problem = false;
+  rc = prepare(c, h);
+  if (rc) return rc;
+  cudaStream_t s = c->stream;
+  rc = copy_small(c, h, s);
+  if (rc) return rc;
+  rc = copy_rows(c, h, 0, ncouls, s);
+  if (rc) return rc;
+  GPP_CUDA(cudaStreamSynchronize(s));
+  c->have_problem = true;
+  return GPP_OK;
+}
+
+int gpp_evaluate_host(gpp_ctx* c, int32_t variant, int64_t nbands, int64_t ngpown, int64_t ncouls,
+                      int32_t nw, const double* wtilde, const double* i_eps,
+                      const double* aqsntemp, const double* aqsmtemp, const double* wx,
+                      int32_t wx_band_indexed, int64_t band0, int64_t band1, int32_t slabs,
+                      double* achtemp, double* asxtemp, int64_t* near_far, float* ms) {
+  const HostProblem h{nbands, ngpown, ncouls, nw, wtilde, i_eps, aqsntemp, aqsmtemp, wx,
+                      wx_band_indexed, band0, band1};
+  int rc = validate(c, h);
+  if (rc) return rc;
+  rc = check_variant(variant);
+  if (rc) return rc;
+  if (!achtemp || !asxtemp) return fail(GPP_ERR_ARG, "output pointer is NULL");
+  rc = ensure_init(c);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
+  if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+  c->have_problem = false;
+  rc = prepare(c, h);
+  if (rc) return rc;
+  // ig slabs on 256-ig block boundaries.
+  const int n_blk = static_cast<int>((ncouls + gpp::kThreads - 1) / gpp::kThreads);
+  const int n_sl = std::max(1, std::min<int>(slabs > 0 ? slabs : 16, n_blk));
+  while (static_cast<int>(c->slab_ev.size()) < n_sl + 1) {
+    cudaEvent_t e;
+    GPP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->slab_ev.push_back(e);
+  }
+  SlabSched sched;
+  for (int sl = 0; sl <= n_sl; ++sl) sched.blk0.push_back(static_cast<int>(
+      static_cast<int64_t>(n_blk) * sl / n_sl));
+  // Copy stream: small arrays, then the ig rows slab by slab, each slab
+  // signalling the compute stream; the compute stream runs slab s while the
+  // rows of slab s+1 are in flight.
+  GPP_CUDA(cudaEventRecord(c->ev[2], c->cstream));
+  rc = copy_small(c, h, c->cstream);
+  if (rc) return rc;
+  for (int sl = 0; sl < n_sl; ++sl) {
+    const int64_t i0 = static_cast<int64_t>(sched.blk0[sl]) * gpp::kThreads;
+    const int64_t i1 = std::min<int64_t>(ncouls, static_cast<int64_t>(sched.blk0[sl + 1]) * gpp::kThreads);
+    rc = copy_rows(c, h, i0, i1, c->cstream);
+    if (rc) return rc;
+    GPP_CUDA(cudaEventRecord(c->slab_ev[sl], c->cstream));
+    sched.ready.push_back(c->slab_ev[sl]);
+  }
+  rc = enqueue_eval(c, variant, near_far != nullptr, nullptr, false, &sched);
+  if (rc) return rc;
+  GPP_CUDA(cudaEventRecord(c->ev[3], c->stream));
+  rc = finish_run(c, achtemp, asxtemp, near_far);
+  if (rc) return rc;
+  c->have_problem = true;
+  if (ms) GPP_CUDA(cudaEventElapsedTime(ms, c->ev[2], c->ev[3]));
+  return GPP_OK;
+}
+
+int gpp_run(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp, int64_t* near_far,
+            float* kernel_ms) {
+  if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
+  int rc = check_variant(variant);
+  if (rc) return rc;
+  if (!achtemp || !asxtemp) return fail(GPP_ERR_ARG, "output pointer is NULL");
+  if (!c->have_problem) return fail(GPP_ERR_ARG, "no problem uploaded");
+  DeviceGuard g(c->device);
+  if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+  GPP_CUDA(cudaEventRecord(c->ev[2], c->stream));
+  rc = enqueue_eval(c, variant, near_far != nullptr, nullptr, false);
+  if (rc) return rc;
+  GPP_CUDA(cudaEventRecord(c->ev[3], c->stream));
+  rc = finish_run(c, achtemp, asxtemp, near_far);
+  if (rc) return rc;
   if (kernel_ms) GPP_CUDA(cudaEventElapsedTime(kernel_ms, c->ev[2], c->ev[3]));
   return GPP_OK;
 }

@@ -90,9 +90,7 @@ class GPPContext:
             pass
 
     # -- data --------------------------------------------------------------
-    def upload(self, problem, band_range: tuple[int, int] | None = None, force: bool = False):
-        """Copy ``problem`` (or its band shard) to the device unless cached."""
-        arrays = prepare_arrays(problem)
+    def _make_key(self, problem, arrays, band_range):
         nb = int(problem.nbands)
         b0, b1 = (0, nb) if band_range is None else (int(band_range[0]), int(band_range[1]))
         key = (
@@ -101,23 +99,70 @@ class GPPContext:
             (b0, b1),
         )
         cacheable = all(not a.flags.writeable for a in arrays.values())
+        return key, cacheable, (b0, b1)
+
+    def _remember(self, problem, arrays, key, cacheable, br):
+        self.nw = int(arrays["wx"].shape[0])
+        self.band_range = br
+        self.dims = (int(problem.nbands), int(problem.ngpown), int(problem.ncouls))
+        self._key = key if cacheable else None
+        self._keep = arrays if cacheable else None  # pin ids while cached
+
+    def is_resident(self, problem, band_range: tuple[int, int] | None = None) -> bool:
+        """Whether ``problem`` (read-only arrays) is already on the device."""
+        arrays = prepare_arrays(problem)
+        key, cacheable, _ = self._make_key(problem, arrays, band_range)
+        return cacheable and key == self._key
+
+    def upload(self, problem, band_range: tuple[int, int] | None = None, force: bool = False):
+        """Copy ``problem`` (or its band shard) to the device unless cached."""
+        arrays = prepare_arrays(problem)
+        key, cacheable, (b0, b1) = self._make_key(problem, arrays, band_range)
         if not force and cacheable and key == self._key:
             return
+        self._key = None
         wx = arrays["wx"]
         _lib.check(
             self._lib.gpp_upload(
-                self._h, nb, int(problem.ngpown), int(problem.ncouls), int(wx.shape[0]),
+                self._h, int(problem.nbands), int(problem.ngpown), int(problem.ncouls), int(wx.shape[0]),
                 _lib.dptr(arrays["wtilde"]), _lib.dptr(arrays["i_eps"]),
                 _lib.dptr(arrays["aqsntemp"]), _lib.dptr(arrays["aqsmtemp"]),
                 _lib.dptr(wx), 1 if wx.ndim == 2 else 0, b0, b1,
             ),
             "gpp_upload",
         )
-        self.nw = int(wx.shape[0])
-        self.band_range = (b0, b1)
-        self.dims = (nb, int(problem.ngpown), int(problem.ncouls))
-        self._key = key if cacheable else None
-        self._keep = arrays if cacheable else None  # pin ids while cached
+        self._remember(problem, arrays, key, cacheable, (b0, b1))
+
+    def evaluate_host(self, problem, variant: str = "rcp_sq",
+                      band_range: tuple[int, int] | None = None, counts: bool = False,
+                      slabs: int = 0):
+        """Upload + evaluate with the H2D copy pipelined against the kernel
+        (gpp_evaluate_host): (GPPResult, (near, far) | None, device_ms)."""
+        code = _variant_code(variant)
+        arrays = prepare_arrays(problem)
+        key, cacheable, (b0, b1) = self._make_key(problem, arrays, band_range)
+        self._key = None
+        wx = arrays["wx"]
+        nw = int(wx.shape[0])
+        ach = np.empty(2 * nw, dtype=np.float64)
+        asx = np.empty(2 * nw, dtype=np.float64)
+        nf = np.zeros(2, dtype=np.int64)
+        ms = ctypes.c_float()
+        nf_ptr = nf.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)) if counts else None
+        _lib.check(
+            self._lib.gpp_evaluate_host(
+                self._h, code, int(problem.nbands), int(problem.ngpown), int(problem.ncouls), nw,
+                _lib.dptr(arrays["wtilde"]), _lib.dptr(arrays["i_eps"]),
+                _lib.dptr(arrays["aqsntemp"]), _lib.dptr(arrays["aqsmtemp"]),
+                _lib.dptr(wx), 1 if wx.ndim == 2 else 0, b0, b1, int(slabs),
+                _lib.dptr(ach), _lib.dptr(asx), nf_ptr, ctypes.byref(ms),
+            ),
+            "gpp_evaluate_host",
+        )
+        self._remember(problem, arrays, key, cacheable, (b0, b1))
+        result = GPPResult(achtemp=ach.view(np.complex128).copy(),
+                           asxtemp=asx.view(np.complex128).copy())
+        return result, ((int(nf[0]), int(nf[1])) if counts else None), float(ms.value)
 
     def run(self, variant: str = "rcp_sq", counts: bool = True):
         """Evaluate the uploaded problem: (GPPResult, (near, far) | None, kernel_ms).
@@ -184,8 +229,10 @@ def get_context(device: int = 0) -> GPPContext:
 def evaluate(problem, variant: str = "rcp_sq", device: int = 0, counts: bool = True):
     """Upload (cached) + run: (GPPResult, BranchStats | None, kernel_ms)."""
     ctx = get_context(device)
-    ctx.upload(problem)
-    result, nf, ms = ctx.run(variant, counts=counts)
+    if ctx.is_resident(problem):
+        result, nf, ms = ctx.run(variant, counts=counts)
+    else:  # first sight of these arrays: pipelined upload + evaluation
+        result, nf, ms = ctx.evaluate_host(problem, variant, counts=counts)
     stats = None
     if nf is not None:
         nb, ng, nc = ctx.dims

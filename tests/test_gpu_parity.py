@@ -138,10 +138,22 @@ def _run(p, band_range):
 
 
 def test_deterministic_bitwise():
+    """Static item schedules: the same path gives the same bits.  (The
+    pipelined first call sums per ig slab, a different -- equally fixed --
+    order than the resident single launch.)"""
     p = synth_problem(128, 66, 4096, seed=1, nw=3)
-    a = evaluate_variant(p, "rcp_sq")
+    first = evaluate_variant(p, "rcp_sq")          # pipelined upload + evaluate
+    a = evaluate_variant(p, "rcp_sq")              # resident
     b = evaluate_variant(p, "rcp_sq")
     assert np.array_equal(a.achtemp, b.achtemp) and np.array_equal(a.asxtemp, b.asxtemp)
+    assert max_rel_error(first, a) <= 1e-13
+    ctx = GPPContext(0)
+    try:
+        c = ctx.evaluate_host(p, "rcp_sq")[0]
+        d = ctx.evaluate_host(p, "rcp_sq")[0]
+        assert np.array_equal(c.achtemp, d.achtemp) and np.array_equal(c.asxtemp, d.asxtemp)
+    finally:
+        ctx.close()
 
 
 def test_writeable_inputs_are_reuploaded():
@@ -202,3 +214,25 @@ def test_irregular_items_take_the_general_path():
     for r in (got, evaluate_variant(q, "rcp_sq")):
         assert np.all(np.isfinite(r.achtemp)) and np.all(np.isfinite(r.asxtemp))
         assert max_rel_error(r, want) <= TOL
+
+
+@pytest.mark.parametrize("slabs", [1, 3, 8, 1000])
+def test_pipelined_host_evaluate(slabs):
+    """gpp_evaluate_host: H2D by ig slabs overlapped with the kernel; same
+    result as upload + run (bitwise: same items, same partial order per slab
+    set), and ragged ncouls (not a multiple of 256)."""
+    p = synth_problem(40, 9, 1000, seed=1, nw=3)
+    want = orc.reference_result(p)
+    ctx = GPPContext(0)
+    try:
+        got, nf, ms = ctx.evaluate_host(p, "rcp_sq", counts=True, slabs=slabs)
+        assert max_rel_error(got, want) <= TOL
+        inst, near, far = orc.branch_stats(p, "rcp_sq")
+        assert nf == (near, far)
+        again, _, _ = ctx.run("rcp_sq", counts=False)  # now resident
+        assert max_rel_error(again, want) <= TOL
+        part, _, _ = ctx.evaluate_host(p, "rcp_sq", band_range=(10, 30), slabs=slabs)
+        ref = orc.reference_result(__import__("paper_2008_11326_b200.dist", fromlist=["x"]).shard_problem(p, 10, 30))
+        assert max_rel_error(part, ref) <= TOL
+    finally:
+        ctx.close()
