@@ -233,14 +233,14 @@ FinalizeFn pick_finalize(int nw) {
   }
 }
 
-// igp tile for the fast kernel: the size in {4, 3} wasting the fewest padded
-// igp columns, ties to 4.
+// igp tile for the fast kernel: 3 or 4 igp per thread.  Padded igp columns
+// cost full work, and the 4-wide tile runs ~5 % slower per instance under the
+// 128-register budget (tools/sweep.py, profiles/r01_sweep.jsonl), so pick the
+// smaller padded cost with that weight.
 int choose_igp_tile(int64_t ngpown) {
-  int best = 4;
-  int64_t best_waste = (ngpown + 3) / 4 * 4 - ngpown;
-  const int64_t w3 = (ngpown + 2) / 3 * 3 - ngpown;
-  if (w3 < best_waste) best = 3;
-  return best;
+  const double cost3 = static_cast<double>((ngpown + 2) / 3 * 3);
+  const double cost4 = 1.05 * static_cast<double>((ngpown + 3) / 4 * 4);
+  return cost4 < cost3 ? 4 : 3;
 }
 
 int make_plan(gpp_ctx* c, int variant, int nw_group, bool count, Plan* pl) {
