@@ -103,3 +103,11 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def dump(path, name, lo, hi):
+    """Per-instruction RF cost listing (debug aid)."""
+    for a, body in load(path, name):
+        if lo <= a <= hi:
+            b = body[body.index(" ") + 1:] if body.startswith("@") else body
+            print(f"{a:05x} {cost(b.split()[0], b)}  {body}")
