@@ -56,6 +56,18 @@ extern "C" {
 #define GPP_VARIANT_RCP 1
 #define GPP_VARIANT_RCP_SQ 2
 
+/* Intermediate rcp_sq kernels of the B200 version ladder (the paper's
+ * optimisation steps re-derived, rooflab/gpp/runner.py:75-115); same results
+ * as GPP_VARIANT_RCP_SQ, kept so each step can be measured:
+ *   SQ_SPLIT  squared-magnitude predicates as integer compares, separate
+ *             MUFU seeds for 1/d and sqrt, per-instance y    (paper v3-v4)
+ *   IW_HOIST  eps*t, wt*(eps*t), |wt|^2 (eps*t) formed once per (band, igp,
+ *             ig) and reused across frequencies              (paper v5-v7)
+ * GPP_VARIANT_RCP_SQ is the final kernel (single rsqrt seed for 1/d and
+ * sqrt(d), regular-item fast path; paper v8). */
+#define GPP_KERNEL_SQ_SPLIT 3
+#define GPP_KERNEL_IW_HOIST 4
+
 typedef struct gpp_ctx gpp_ctx;
 
 /* ABI revision (GPP_ABI_VERSION) of the loaded library. */

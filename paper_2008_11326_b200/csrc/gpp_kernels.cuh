@@ -152,53 +152,6 @@ __device__ __forceinline__ void select_branches(double d, long long qbits, doubl
   }
 }
 
-// Seed selection (ALG 2): the branch decisions gate the MUFU seeds instead of
-// the refined results.  A zero seed refines to exactly zero (e = 1 - d*0 = 1,
-// r = 0 * (...) = 0), so selecting the seed's high word (the low word of a
-// MUFU.RCP64H / RSQ64H result is zero) costs one 32-bit select per branch
-// instead of a 64-bit select of the refined value.
-template <bool COUNT, int NW>
-__device__ __forceinline__ void gated_seeds(double d, long long qbits, double x, double& rr,
-                                            double& rs, Acc<NW>& acc) {
-  const long long dbits = __double_as_longlong(d);
-  const long long xbits = __double_as_longlong(x);
-  if constexpr (COUNT) {
-    asm("{\n\t.reg .pred pn, pf;\n\t.reg .u64 xm1;\n\t.reg .f64 s0, s1;\n\t"
-        ".reg .b32 l0, h0, l1, h1;\n\t"
-        "setp.gt.s64 pn, %4, %5;\n\t"
-        "sub.u64 xm1, %6, 1;\n\t"
-        "setp.lt.and.u64 pf, xm1, %7, !pn;\n\t"
-        "rcp.approx.ftz.f64 s0, %8;\n\t"
-        "rsqrt.approx.ftz.f64 s1, %9;\n\t"
-        "mov.b64 {l0, h0}, s0;\n\t"
-        "mov.b64 {l1, h1}, s1;\n\t"
-        "selp.b32 h0, h0, 0, pn;\n\t"
-        "selp.b32 h1, h1, 0, pf;\n\t"
-        "mov.b64 %0, {l0, h0};\n\t"
-        "mov.b64 %1, {l1, h1};\n\t"
-        "@pn add.u32 %2, %2, 1;\n\t"
-        "@pf add.u32 %3, %3, 1;\n\t}"
-        : "=d"(rr), "=d"(rs), "+r"(acc.nn), "+r"(acc.nf)
-        : "l"(dbits), "l"(qbits), "l"(xbits), "l"(kBits1e24 - 1ull), "d"(d), "d"(x));
-  } else {
-    asm("{\n\t.reg .pred pn, pf;\n\t.reg .u64 xm1;\n\t.reg .f64 s0, s1;\n\t"
-        ".reg .b32 l0, h0, l1, h1;\n\t"
-        "setp.gt.s64 pn, %2, %3;\n\t"
-        "sub.u64 xm1, %4, 1;\n\t"
-        "setp.lt.and.u64 pf, xm1, %5, !pn;\n\t"
-        "rcp.approx.ftz.f64 s0, %6;\n\t"
-        "rsqrt.approx.ftz.f64 s1, %7;\n\t"
-        "mov.b64 {l0, h0}, s0;\n\t"
-        "mov.b64 {l1, h1}, s1;\n\t"
-        "selp.b32 h0, h0, 0, pn;\n\t"
-        "selp.b32 h1, h1, 0, pf;\n\t"
-        "mov.b64 %0, {l0, h0};\n\t"
-        "mov.b64 %1, {l1, h1};\n\t}"
-        : "=d"(rr), "=d"(rs)
-        : "l"(dbits), "l"(qbits), "l"(xbits), "l"(kBits1e24 - 1ull), "d"(d), "d"(x));
-  }
-}
-
 // sqrt(x) from the MUFU.RSQ64H seed r (rel. error ~2^-20, measured).
 //   STEPS = 1: one coupled Newton step            4 FP64, rel. error ~1e-12
 //   STEPS = 2: two coupled Newton steps           7 FP64, ~1 ulp
@@ -236,11 +189,11 @@ __device__ __forceinline__ double sqrt_nr(double x) {
 //   far   <=> !near && d/|wt|^2 < 1e24
 //   sum a += near * inv * num * (eps t)                   -> ach = a/2
 //   sum b += far  * sqrt(d/|wt|^2) * (eps t)              -> asx = a - b/4
-// ALG 0 forms y = num * (eps t) per instance (6 FP64);  ALG 1/2 form
+// ALG 0 forms y = num * (eps t) per instance (6 FP64);  ALG 1 forms
 // P = wt*(eps t) and Q = |wt|^2 (eps t) once per (band, igp, ig) and then
 // y = wx P - Q per instance (2 DFMA), which pays off from nw = 2 on.
-// ALG 2 additionally gates the MUFU seeds (gated_seeds) instead of selecting
-// the refined multipliers.
+// These are the intermediate kernels of the version ladder
+// (GPP_KERNEL_SQ_SPLIT = <0, 2>, GPP_KERNEL_IW_HOIST = <1, 3>).
 template <int ALG, int SQRT_STEPS>
 struct FastPolicyT {
   struct St {
@@ -295,22 +248,9 @@ struct FastPolicyT {
         yim = fma(nre, eti, nim * etr);
       }
       double in, gf;
-      if constexpr (ALG == 2) {
-        double rr, rs;
-        gated_seeds<COUNT>(d, qbits, x, rr, rs, acc);
-        // 1/d refined from the gated seed (cubic step), sqrt(x) likewise.
-        double e = fma(-d, rr, 1.0);
-        e = fma(e, e, e);
-        in = fma(e, rr, rr);
-        const double t = x * rs;
-        const double es = fma(-t, rs, 1.0);
-        const double ps = fma(es, 0.375, 0.5);
-        gf = fma(t, es * ps, t);
-      } else {
-        const double inv = rcp_refined(d);
-        const double g = sqrt_nr<SQRT_STEPS>(x);
-        select_branches<COUNT>(d, qbits, x, inv, g, in, gf, acc);
-      }
+      const double inv = rcp_refined(d);
+      const double g = sqrt_nr<SQRT_STEPS>(x);
+      select_branches<COUNT>(d, qbits, x, inv, g, in, gf, acc);
       acc.a[iw].x = fma(in, yre, acc.a[iw].x);
       acc.a[iw].y = fma(in, yim, acc.a[iw].y);
       acc.b[iw].x = fma(gf, etr, acc.b[iw].x);

@@ -146,47 +146,36 @@ struct Plan {
 
 using KernelFn = void (*)(gpp::Params);
 
-// Tuning override for experiments: GPP_TUNE="igp,minb,alg,sqrt" selects an
-// alternative register/occupancy trade-off and formulation of the fast kernel
-// (nw 2 or 3 only; 0 keeps the default).
+// Launch-shape override for experiments: GPP_TUNE="igp,bps" forces the igp
+// tile (2..4) of the rcp_sq kernels at nw 2/3 and caps resident CTAs per SM.
+// Unset (the default) the planner chooses.
 struct Tune {
-  int igp = 0, minb = 0, alg = -1, sq = 0, bps = 0;
+  int igp = 0, bps = 0;
 };
 Tune read_tune() {
   Tune t;
   const char* e = std::getenv("GPP_TUNE");
-  if (e) std::sscanf(e, "%d,%d,%d,%d,%d", &t.igp, &t.minb, &t.alg, &t.sq, &t.bps);
+  if (e) std::sscanf(e, "%d,%d", &t.igp, &t.bps);
   return t;
 }
 
 template <class FP, int NW, bool C>
-KernelFn pick_fast_tuned(const Tune& t) {
-  if (t.minb == 3) {
-    if (t.igp == 2) return gpp::gpp_main_kernel<FP, NW, 2, C, 3>;
-    return gpp::gpp_main_kernel<FP, NW, 3, C, 3>;
+KernelFn pick_fast(int igp_t) {
+  if constexpr (NW == 2 || NW == 3) {
+    if (igp_t == 2) return gpp::gpp_main_kernel<FP, NW, 2, C>;
+    if (igp_t == 4) return gpp::gpp_main_kernel<FP, NW, 4, C>;
   }
-  if (t.igp == 2) return gpp::gpp_main_kernel<FP, NW, 2, C>;
-  if (t.igp == 4) return gpp::gpp_main_kernel<FP, NW, 4, C>;
   return gpp::gpp_main_kernel<FP, NW, 3, C>;
 }
 
-template <int NW, bool C>
-KernelFn pick_fast(int igp_t) {
-  if constexpr (NW == 2 || NW == 3) {
-    const Tune t = read_tune();
-    if (t.alg >= 0 || t.minb || t.igp) {
-      if (t.alg == 3) return pick_fast_tuned<gpp::FastPolicy3, NW, C>(t);
-      if (t.alg == 2) return pick_fast_tuned<gpp::FastPolicyT<2, 3>, NW, C>(t);
-      if (t.alg == 1 && t.sq == 1) return pick_fast_tuned<gpp::FastPolicyT<1, 1>, NW, C>(t);
-      if (t.alg == 1 && t.sq == 2) return pick_fast_tuned<gpp::FastPolicyT<1, 2>, NW, C>(t);
-      if (t.alg == 1) return pick_fast_tuned<gpp::FastPolicyT<1, 3>, NW, C>(t);
-      if (t.sq == 1) return pick_fast_tuned<gpp::FastPolicyT<0, 1>, NW, C>(t);
-      if (t.sq == 2) return pick_fast_tuned<gpp::FastPolicyT<0, 2>, NW, C>(t);
-      return pick_fast_tuned<gpp::FastPolicyT<0, 3>, NW, C>(t);
-    }
+template <class FP, bool C>
+KernelFn pick_fast_nw(int nw, int igp_t) {
+  switch (nw) {
+    case 1: return pick_fast<FP, 1, C>(igp_t);
+    case 2: return pick_fast<FP, 2, C>(igp_t);
+    case 3: return pick_fast<FP, 3, C>(igp_t);
+    default: return pick_fast<FP, 4, C>(igp_t);
   }
-  if (NW >= 4 || igp_t == 3) return gpp::gpp_main_kernel<gpp::FastPolicy, NW, 3, C>;
-  return gpp::gpp_main_kernel<gpp::FastPolicy, NW, (NW >= 4 ? 3 : 4), C>;
 }
 
 template <class P, bool C>
@@ -204,13 +193,9 @@ KernelFn pick_kernel_c(int variant, int nw, int igp_t) {
   switch (variant) {
     case GPP_VARIANT_DIV: return pick_plain<gpp::PlainPolicy<0>, C>(nw);
     case GPP_VARIANT_RCP: return pick_plain<gpp::PlainPolicy<1>, C>(nw);
-    default:
-      switch (nw) {
-        case 1: return pick_fast<1, C>(igp_t);
-        case 2: return pick_fast<2, C>(igp_t);
-        case 3: return pick_fast<3, C>(igp_t);
-        default: return pick_fast<4, C>(igp_t);
-      }
+    case GPP_KERNEL_SQ_SPLIT: return pick_fast_nw<gpp::FastPolicyT<0, 2>, C>(nw, igp_t);
+    case GPP_KERNEL_IW_HOIST: return pick_fast_nw<gpp::FastPolicyT<1, 3>, C>(nw, igp_t);
+    default: return pick_fast_nw<gpp::FastPolicy, C>(nw, igp_t);
   }
 }
 
@@ -247,12 +232,12 @@ int make_plan(gpp_ctx* c, int variant, int nw_group, bool count, Plan* pl) {
   // The plain (as-written) variants keep two igp per thread and the fast
   // kernel drops to 3 at four frequencies: both choices avoid spills under
   // the 128-register budget of __launch_bounds__(256, 2).
-  if (variant != GPP_VARIANT_RCP_SQ)
+  if (variant == GPP_VARIANT_DIV || variant == GPP_VARIANT_RCP)
     pl->igp_t = 2;
   else
     pl->igp_t = nw_group >= 4 ? 3 : choose_igp_tile(c->ngpown);
   const Tune tune = read_tune();
-  if (variant == GPP_VARIANT_RCP_SQ && (nw_group == 2 || nw_group == 3) && tune.igp >= 2 &&
+  if (variant >= GPP_VARIANT_RCP_SQ && (nw_group == 2 || nw_group == 3) && tune.igp >= 2 &&
       tune.igp <= 4)
     pl->igp_t = tune.igp;
   pl->n_igblk = static_cast<int>((c->ncouls + gpp::kThreads - 1) / gpp::kThreads);
@@ -347,7 +332,7 @@ int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool
     }
     if (ev_main && gi + 1 == groups.size()) GPP_CUDA(cudaEventRecord(ev_main[1], c->stream));
     pick_finalize(nwg)<<<1, 256, 0, c->stream>>>(c->partials.ptr, c->cpartials.ptr, rows,
-                                                  c->nw, iw0, variant == GPP_VARIANT_RCP_SQ,
+                                                  c->nw, iw0, variant >= GPP_VARIANT_RCP_SQ,
                                                   first ? 1 : 0, count ? 1 : 0, c->out.ptr,
                                                   c->counts.ptr);
     GPP_CUDA(cudaGetLastError());
@@ -365,9 +350,9 @@ int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool
 }
 
 int check_variant(int32_t variant) {
-  if (variant < GPP_VARIANT_DIV || variant > GPP_VARIANT_RCP_SQ)
+  if (variant < GPP_VARIANT_DIV || variant > GPP_KERNEL_IW_HOIST)
     return fail(GPP_ERR_ARG, "unknown variant " + std::to_string(variant) +
-                                 " (expected 0=div, 1=rcp, 2=rcp_sq)");
+                                 " (expected 0=div, 1=rcp, 2=rcp_sq, 3/4 = ladder kernels)");
   return GPP_OK;
 }
 

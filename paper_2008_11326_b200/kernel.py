@@ -57,9 +57,17 @@ def prepare_arrays(problem) -> dict[str, np.ndarray]:
 
 
 def _variant_code(variant: str) -> int:
+    """Code of a reference variant (div / rcp / rcp_sq) or of one of the
+    intermediate ladder kernels ("rcp_sq/split", "rcp_sq/iw")."""
+    code = _lib.KERNEL_CODES.get(variant)
+    if code is None:
+        raise DomainError(f"unknown variant {variant!r}, expected one of {VARIANTS}")
+    return code
+
+
+def _reference_variant(variant: str) -> None:
     if variant not in VARIANTS:
         raise DomainError(f"unknown variant {variant!r}, expected one of {VARIANTS}")
-    return _lib.VARIANT_CODES[variant]
 
 
 class GPPContext:
@@ -242,13 +250,13 @@ def evaluate(problem, variant: str = "rcp_sq", device: int = 0, counts: bool = T
 
 def evaluate_variant(problem, variant: str, device: int = 0) -> GPPResult:
     """Drop-in for rooflab.gpp.kernel.evaluate_variant (kernel.py:98-114)."""
-    _variant_code(variant)
+    _reference_variant(variant)
     return evaluate(problem, variant, device, counts=False)[0]
 
 
 def branch_stats(problem, variant: str, device: int = 0) -> BranchStats:
     """Drop-in for rooflab.gpp.kernel.branch_stats (kernel.py:130-137)."""
-    _variant_code(variant)
+    _reference_variant(variant)
     return evaluate(problem, variant, device)[1]
 
 

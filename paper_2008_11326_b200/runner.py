@@ -75,6 +75,23 @@ VERSIONS: dict[str, VersionSpec] = {
 }
 VERSION_NAMES = tuple(VERSIONS)
 
+# The B200 ladder: which CUDA kernel re-derives each version's step
+# (include/gpp_b200.h).  The reference's traversal-only versions (v2, v4, v6,
+# v7) share the kernel of the arithmetic they keep; B200's traversal (thread
+# <-> ig, band innermost, aqsmtemp/wx staged in shared memory, cp.async
+# aqsntemp ring) is common to all kernels.
+B200_KERNEL = {
+    "v0": "div",            # library complex division, |.| predicates
+    "v1": "rcp",            # reciprocal times multiply
+    "v2": "rcp",            # branch bodies folded (predication: already so)
+    "v3": "rcp_sq/split",   # squared predicates (integer compares), MUFU seeds
+    "v4": "rcp_sq/split",   # band innermost (all B200 kernels)
+    "v5": "rcp_sq/iw",      # per-tuple eps*t, P, Q reused across iw
+    "v6": "rcp_sq/iw",      # cache blocking (smem staging, cp.async ring)
+    "v7": "rcp_sq/iw",      # aqsmtemp tile transposed in shared memory
+    "v8": "rcp_sq",         # single rsqrt seed, regular-item fast path, tuned occupancy
+}
+
 
 def version_spec(name: str) -> VersionSpec:
     try:
@@ -101,6 +118,7 @@ class RunArtifacts:
     version: str
     dims: tuple[int, int, int]
     variant: str
+    kernel: str
     result: GPPResult
     counters: InstructionCounters
     stats: BranchStats
@@ -124,9 +142,10 @@ def run_version(problem, name: str, trace: bool = False, contraction: bool = Tru
     # Timed like the reference (runner.py:258-260): the evaluation alone; the
     # branch statistics come from a second, counting launch (kernel.py:262
     # computes them in a separate pass too).
+    kernel = B200_KERNEL[name]
     start = time.perf_counter()
     ctx.upload(problem)
-    result, _, kernel_ms = ctx.run(spec.variant, counts=False)
+    result, _, kernel_ms = ctx.run(kernel, counts=False)
     elapsed = time.perf_counter() - start
     _, (near, far), _ = ctx.run(spec.variant, counts=True)
     nb, ng, nc = ctx.dims
@@ -134,12 +153,13 @@ def run_version(problem, name: str, trace: bool = False, contraction: bool = Tru
     stats = BranchStats(instances=ctx.nw * tuples, near=near, far=far)
     t_products = tuples * (ctx.nw if spec.t_per_instance else 1)
     counters = counters_from_stats(spec.variant, stats, t_products, spec.far_takes_sqrt, contraction)
-    info = ctx.kernel_info(spec.variant)
+    info = ctx.kernel_info(kernel)
     warps = info["blocks_per_sm"] * info["threads_per_block"] // WARP_SIZE
     return RunArtifacts(
         version=name,
         dims=(nb, ng, nc),
         variant=spec.variant,
+        kernel=kernel,
         result=result,
         counters=counters,
         stats=stats,

@@ -236,3 +236,28 @@ def test_pipelined_host_evaluate(slabs):
         assert max_rel_error(part, ref) <= TOL
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("kernel", ["rcp_sq/split", "rcp_sq/iw"])
+def test_ladder_kernels_vs_reference(kernel):
+    """The intermediate kernels of the B200 version ladder give the reference's
+    results and exact counts too."""
+    ctx = GPPContext(0)
+    try:
+        for case in [c for c in SMALL if c["dims"] in ([47, 2, 33], [64, 64, 512], [32, 8, 512])]:
+            p = synth_problem(*case["dims"], seed=case["seed"], nw=case["nw"])
+            ctx.upload(p)
+            got, nf, _ = ctx.run(kernel, counts=True)
+            assert max_rel_error(got, _R(case["reference_result"])) <= TOL
+            assert [case["nw"] * np.prod(case["dims"]), *nf] == case["branch_stats"]["rcp_sq"]
+            fast, _, _ = ctx.run(kernel, counts=False)
+            assert max_rel_error(fast, _R(case["reference_result"])) <= TOL
+    finally:
+        ctx.close()
+
+
+def test_evaluate_variant_rejects_ladder_names():
+    from paper_2008_11326_b200.errors import DomainError
+
+    with pytest.raises(DomainError):
+        evaluate_variant(synth_problem(2, 2, 16, seed=5), "rcp_sq/iw")
