@@ -159,11 +159,22 @@ Tune read_tune() {
   return t;
 }
 
+// The igp tile actually instantiated for a frequency group: 3 or 4 igp per
+// thread below four frequencies (2 only as a GPP_TUNE experiment at nw 2/3),
+// 3 at four (the 4x4 state does not fit 128 registers).
+int fast_igp(int nw, int igp_t) {
+  if (nw >= 4) return 3;
+  if (igp_t == 2) return (nw == 2 || nw == 3) ? 2 : 3;
+  return igp_t == 4 ? 4 : 3;
+}
+
 template <class FP, int NW, bool C>
 KernelFn pick_fast(int igp_t) {
+  if constexpr (NW < 4) {
+    if (igp_t == 4) return gpp::gpp_main_kernel<FP, NW, 4, C>;
+  }
   if constexpr (NW == 2 || NW == 3) {
     if (igp_t == 2) return gpp::gpp_main_kernel<FP, NW, 2, C>;
-    if (igp_t == 4) return gpp::gpp_main_kernel<FP, NW, 4, C>;
   }
   return gpp::gpp_main_kernel<FP, NW, 3, C>;
 }
@@ -232,14 +243,12 @@ int make_plan(gpp_ctx* c, int variant, int nw_group, bool count, Plan* pl) {
   // The plain (as-written) variants keep two igp per thread and the fast
   // kernel drops to 3 at four frequencies: both choices avoid spills under
   // the 128-register budget of __launch_bounds__(256, 2).
-  if (variant == GPP_VARIANT_DIV || variant == GPP_VARIANT_RCP)
-    pl->igp_t = 2;
-  else
-    pl->igp_t = nw_group >= 4 ? 3 : choose_igp_tile(c->ngpown);
   const Tune tune = read_tune();
-  if (variant >= GPP_VARIANT_RCP_SQ && (nw_group == 2 || nw_group == 3) && tune.igp >= 2 &&
-      tune.igp <= 4)
-    pl->igp_t = tune.igp;
+  if (variant == GPP_VARIANT_DIV || variant == GPP_VARIANT_RCP)
+    pl->igp_t = 2;  // the only instantiation of the plain kernels
+  else
+    pl->igp_t = fast_igp(nw_group, tune.igp >= 2 && tune.igp <= 4 ? tune.igp
+                                                                  : choose_igp_tile(c->ngpown));
   pl->n_igblk = static_cast<int>((c->ncouls + gpp::kThreads - 1) / gpp::kThreads);
   pl->n_igptile = static_cast<int>((c->ngpown + pl->igp_t - 1) / pl->igp_t);
   KernelFn fn = pick_kernel(variant, nw_group, pl->igp_t, count);
