@@ -147,6 +147,15 @@ int gpp_kernel_info(gpp_ctx* ctx, int32_t variant, int32_t* registers_per_thread
 int gpp_comm_unique_id(unsigned char* id128);
 int gpp_comm_init(gpp_ctx* ctx, int nranks, int rank, const unsigned char* id128);
 
+/* Single-process multi-GPU (the survey's ncclCommInitAll design): one
+ * context per device in ONE process, all in one NCCL clique.  Upload each
+ * context's band shard with gpp_upload(..., band0, band1), then
+ * gpp_run_group evaluates every shard, combines the partials with one grouped
+ * ncclAllReduce and returns the totals (kernel_ms = slowest device). */
+int gpp_comm_init_all(gpp_ctx** ctxs, int n);
+int gpp_run_group(gpp_ctx** ctxs, int n, int32_t variant, double* achtemp, double* asxtemp,
+                  int64_t* near_far, float* kernel_ms);
+
 /* Page-lock an existing host buffer so uploads from it run at DMA speed. */
 int gpp_host_register(void* ptr, size_t bytes);
 int gpp_host_unregister(void* ptr);

@@ -736,6 +736,98 @@ int gpp_comm_init(gpp_ctx* c, int nranks, int rank, const unsigned char* id128) 
   return GPP_OK;
 }
 
+int gpp_comm_init_all(gpp_ctx** ctxs, int n) {
+  if (!ctxs || n < 1) return fail(GPP_ERR_ARG, "need at least one context");
+  std::vector<int> devs(n);
+  for (int i = 0; i < n; ++i) {
+    if (!ctxs[i]) return fail(GPP_ERR_ARG, "context " + std::to_string(i) + " is NULL");
+    for (int j = 0; j < i; ++j)
+      if (ctxs[j]->device == ctxs[i]->device)
+        return fail(GPP_ERR_ARG, "contexts must be on distinct devices");
+    int rc = ensure_init(ctxs[i]);
+    if (rc) return rc;
+    devs[i] = ctxs[i]->device;
+    if (ctxs[i]->comm) {
+      DeviceGuard g(ctxs[i]->device);
+      ncclCommDestroy(ctxs[i]->comm);
+      ctxs[i]->comm = nullptr;
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    ctxs[i]->nranks = n;
+    ctxs[i]->rank = i;
+  }
+  if (n == 1) return GPP_OK;
+  std::vector<ncclComm_t> comms(n);
+  GPP_NCCL(ncclCommInitAll(comms.data(), n, devs.data()));
+  for (int i = 0; i < n; ++i) ctxs[i]->comm = comms[i];
+  return GPP_OK;
+}
+
+int gpp_run_group(gpp_ctx** ctxs, int n, int32_t variant, double* achtemp, double* asxtemp,
+                  int64_t* near_far, float* kernel_ms) {
+  if (!ctxs || n < 1) return fail(GPP_ERR_ARG, "need at least one context");
+  int rc = check_variant(variant);
+  if (rc) return rc;
+  if (!achtemp || !asxtemp) return fail(GPP_ERR_ARG, "output pointer is NULL");
+  for (int i = 0; i < n; ++i) {
+    if (!ctxs[i] || !ctxs[i]->have_problem)
+      return fail(GPP_ERR_ARG, "context " + std::to_string(i) + " has no problem uploaded");
+    if (ctxs[i]->nw != ctxs[0]->nw)
+      return fail(GPP_ERR_ARG, "contexts hold problems with different nw");
+    if (n > 1 && (!ctxs[i]->comm || ctxs[i]->nranks != n))
+      return fail(GPP_ERR_ARG, "contexts need gpp_comm_init_all over the same group");
+  }
+  // Every device's shard first, then one grouped allreduce across them (a
+  // single thread must issue all ranks' collectives inside one group).
+  for (int i = 0; i < n; ++i) {
+    gpp_ctx* c = ctxs[i];
+    DeviceGuard g(c->device);
+    if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+    GPP_CUDA(cudaEventRecord(c->ev[2], c->stream));
+    rc = enqueue_eval(c, variant, near_far != nullptr, nullptr, false);
+    if (rc) return rc;
+    GPP_CUDA(cudaEventRecord(c->ev[3], c->stream));
+  }
+  if (n > 1) {
+    GPP_NCCL(ncclGroupStart());
+    for (int i = 0; i < n; ++i) {
+      gpp_ctx* c = ctxs[i];
+      GPP_NCCL(ncclAllReduce(c->out.ptr, c->out.ptr, 4 * c->nw, ncclDouble, ncclSum, c->comm,
+                             c->stream));
+      GPP_NCCL(ncclAllReduce(c->counts.ptr, c->counts.ptr, 2, ncclUint64, ncclSum, c->comm,
+                             c->stream));
+    }
+    GPP_NCCL(ncclGroupEnd());
+  }
+  float worst = 0.f;
+  for (int i = 0; i < n; ++i) {
+    gpp_ctx* c = ctxs[i];
+    DeviceGuard g(c->device);
+    if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+    GPP_CUDA(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    GPP_CUDA(cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
+    worst = std::max(worst, ms);
+  }
+  gpp_ctx* c0 = ctxs[0];
+  {
+    DeviceGuard g(c0->device);
+    if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+    GPP_CUDA(cudaMemcpy(c0->h_out, c0->out.ptr, 4 * sizeof(double) * c0->nw, cudaMemcpyDeviceToHost));
+    GPP_CUDA(cudaMemcpy(c0->h_counts, c0->counts.ptr, 2 * sizeof(unsigned long long),
+                        cudaMemcpyDeviceToHost));
+  }
+  std::memcpy(achtemp, c0->h_out, 2 * sizeof(double) * c0->nw);
+  std::memcpy(asxtemp, c0->h_out + 2 * c0->nw, 2 * sizeof(double) * c0->nw);
+  if (near_far) {
+    near_far[0] = static_cast<int64_t>(c0->h_counts[0]);
+    near_far[1] = static_cast<int64_t>(c0->h_counts[1]);
+  }
+  if (kernel_ms) *kernel_ms = worst;
+  return GPP_OK;
+}
+
 int gpp_host_register(void* ptr, size_t bytes) {
   if (!ptr || bytes == 0) return fail(GPP_ERR_ARG, "empty host range");
   GPP_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));

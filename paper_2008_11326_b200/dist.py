@@ -84,3 +84,52 @@ class ShardedGPP:
 
     def close(self) -> None:
         self.ctx.close()
+
+
+class MultiDeviceGPP:
+    """Single-process band sharding over several local GPUs (SURVEY.md
+    section 2, native component 3): one context per device in one NCCL clique
+    (ncclCommInitAll), every shard launched from this thread, one grouped
+    ncclAllReduce of the partials (gpp_run_group)."""
+
+    def __init__(self, devices):
+        import ctypes
+
+        from . import _lib
+
+        self.devices = [int(d) for d in devices]
+        if not self.devices or len(set(self.devices)) != len(self.devices):
+            raise ValueError("devices must be a non-empty list of distinct device ids")
+        self._lib = _lib.load()
+        self.ctxs = [GPPContext(d) for d in self.devices]
+        self._arr = (ctypes.c_void_p * len(self.ctxs))(*[c._h.value for c in self.ctxs])
+        _lib.check(self._lib.gpp_comm_init_all(self._arr, len(self.ctxs)), "gpp_comm_init_all")
+
+    def upload(self, problem, force: bool = False) -> None:
+        n = len(self.ctxs)
+        for rank, ctx in enumerate(self.ctxs):
+            ctx.upload(problem, band_range(int(problem.nbands), n, rank), force=force)
+
+    def run(self, variant: str = "rcp_sq", counts: bool = True):
+        """(GPPResult, (near, far) | None, slowest-device kernel ms) of the whole problem."""
+        import ctypes
+
+        from . import _lib
+        from .kernel import _variant_code
+        from .problem import GPPResult
+
+        nw = self.ctxs[0].nw
+        ach = np.empty(2 * nw)
+        asx = np.empty(2 * nw)
+        nf = np.zeros(2, dtype=np.int64)
+        ms = ctypes.c_float()
+        nf_ptr = nf.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)) if counts else None
+        _lib.check(self._lib.gpp_run_group(self._arr, len(self.ctxs), _variant_code(variant),
+                                           _lib.dptr(ach), _lib.dptr(asx), nf_ptr, ctypes.byref(ms)),
+                   "gpp_run_group")
+        result = GPPResult(achtemp=ach.view(np.complex128).copy(), asxtemp=asx.view(np.complex128).copy())
+        return result, ((int(nf[0]), int(nf[1])) if counts else None), float(ms.value)
+
+    def close(self) -> None:
+        for c in self.ctxs:
+            c.close()

@@ -261,3 +261,30 @@ def test_evaluate_variant_rejects_ladder_names():
 
     with pytest.raises(DomainError):
         evaluate_variant(synth_problem(2, 2, 16, seed=5), "rcp_sq/iw")
+
+
+def test_single_process_group_api():
+    """gpp_comm_init_all + gpp_run_group over the visible devices (one on the
+    test boxes): the grouped path returns the whole problem's result."""
+    import ctypes
+
+    from paper_2008_11326_b200 import _lib
+    from paper_2008_11326_b200.dist import MultiDeviceGPP
+
+    n = ctypes.c_int()
+    _lib.load().gpp_device_count(ctypes.byref(n))
+    devices = list(range(min(n.value, 8)))
+    p = synth_problem(37, 9, 600, seed=7, nw=3)
+    want = orc.reference_result(p)
+    inst, near, far = orc.branch_stats(p, "rcp_sq")
+    g = MultiDeviceGPP(devices)
+    try:
+        g.upload(p)
+        got, nf, ms = g.run("rcp_sq", counts=True)
+        assert max_rel_error(got, want) <= TOL and nf == (near, far) and ms > 0
+        fast, _, _ = g.run("rcp_sq", counts=False)
+        assert max_rel_error(fast, want) <= TOL
+    finally:
+        g.close()
+    with pytest.raises(ValueError):
+        MultiDeviceGPP([0, 0])
