@@ -49,6 +49,10 @@ SIGNATURES = {
          _c_double_p, _c_double_p, _c_double_p, _c_double_p, _c_double_p, ctypes.c_int32,
          ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _c_double_p, _c_double_p, _c_i64_p, _c_float_p],
     ),
+    "gpp_run_factored": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.c_int32, _c_double_p, _c_double_p, _c_i64_p, _c_float_p],
+    ),
     "gpp_time": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, _c_float_p, _c_float_p]),
     "gpp_kernel_info": (
         ctypes.c_int,

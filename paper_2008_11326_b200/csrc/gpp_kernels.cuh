@@ -463,6 +463,54 @@ struct PlainPolicy {
 // ---------------------------------------------------------------------------
 // Main kernel.
 // ---------------------------------------------------------------------------
+// Deterministic block reduction of the per-thread accumulators: warp xor-tree,
+// then the warps in order; one row of 4*NW doubles (+2 counts, scaled by
+// count_scale) per CTA.
+template <int NW, bool COUNT>
+__device__ __forceinline__ void block_reduce_write(const Acc<NW>& acc, double* partials,
+                                                   unsigned long long* cpartials,
+                                                   unsigned long long count_scale) {
+  __shared__ double s_red[kThreads / 32][4 * NW];
+  __shared__ unsigned long long s_cred[kThreads / 32][2];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  double v[4 * NW];
+#pragma unroll
+  for (int iw = 0; iw < NW; ++iw) {
+    v[4 * iw + 0] = acc.a[iw].x;
+    v[4 * iw + 1] = acc.a[iw].y;
+    v[4 * iw + 2] = acc.b[iw].x;
+    v[4 * iw + 3] = acc.b[iw].y;
+  }
+  unsigned long long cn = acc.nn, cf = acc.nf;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int k = 0; k < 4 * NW; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+    cn += __shfl_xor_sync(0xffffffffu, cn, off);
+    cf += __shfl_xor_sync(0xffffffffu, cf, off);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < 4 * NW; ++k) s_red[warp][k] = v[k];
+    s_cred[warp][0] = cn;
+    s_cred[warp][1] = cf;
+  }
+  __syncthreads();
+  if (tid < 4 * NW) {
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) sum += s_red[w][tid];
+    partials[static_cast<size_t>(blockIdx.x) * (4 * NW) + tid] = sum;
+  } else if (COUNT && tid < 4 * NW + 2) {
+    const int c = tid - 4 * NW;
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) sum += s_cred[w][c];
+    cpartials[static_cast<size_t>(blockIdx.x) * 2 + c] = sum * count_scale;
+  }
+}
+
 // The band loop of one item: aqsntemp streamed through the per-thread
 // cp.async ring, aqsmtemp / wx read from shared memory (uniform broadcasts).
 template <class P, int NW, int IGP_T, bool COUNT, bool FAST>
@@ -502,8 +550,6 @@ template <class P, int NW, int IGP_T, bool COUNT, int MINB = 2>
 __global__ void __launch_bounds__(kThreads, MINB) gpp_main_kernel(const Params p) {
   __shared__ double2 s_am[kMaxChunk][IGP_T];
   __shared__ double s_wx[kMaxChunk][NW];
-  __shared__ double s_red[kThreads / 32][4 * NW];
-  __shared__ unsigned long long s_cred[kThreads / 32][2];
   __shared__ __align__(16) double2 s_an[kAnDepth][kThreads];
 
   Acc<NW> acc;
@@ -564,43 +610,7 @@ __global__ void __launch_bounds__(kThreads, MINB) gpp_main_kernel(const Params p
       band_loop<P, NW, IGP_T, COUNT, false>(anp, p.ncouls, nb, s_an, s_am, s_wx, st, acc);
   }
 
-  // Deterministic block reduction: warp xor-tree, then warps in order.
-  const int lane = tid & 31, warp = tid >> 5;
-  double v[4 * NW];
-#pragma unroll
-  for (int iw = 0; iw < NW; ++iw) {
-    v[4 * iw + 0] = acc.a[iw].x;
-    v[4 * iw + 1] = acc.a[iw].y;
-    v[4 * iw + 2] = acc.b[iw].x;
-    v[4 * iw + 3] = acc.b[iw].y;
-  }
-  unsigned long long cn = acc.nn, cf = acc.nf;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-#pragma unroll
-    for (int k = 0; k < 4 * NW; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
-    cn += __shfl_xor_sync(0xffffffffu, cn, off);
-    cf += __shfl_xor_sync(0xffffffffu, cf, off);
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < 4 * NW; ++k) s_red[warp][k] = v[k];
-    s_cred[warp][0] = cn;
-    s_cred[warp][1] = cf;
-  }
-  __syncthreads();
-  if (tid < 4 * NW) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) s += s_red[w][tid];
-    p.partials[static_cast<size_t>(blockIdx.x) * (4 * NW) + tid] = s;
-  } else if (COUNT && tid < 4 * NW + 2) {
-    const int c = tid - 4 * NW;
-    unsigned long long s = 0;
-#pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) s += s_cred[w][c];
-    p.cpartials[static_cast<size_t>(blockIdx.x) * 2 + c] = s;
-  }
+  block_reduce_write<NW, COUNT>(acc, p.partials, p.cpartials, 1ull);
 }
 
 // Sum the per-CTA partials in a fixed order and form achtemp/asxtemp for the
@@ -666,6 +676,40 @@ __global__ void __launch_bounds__(256) gpp_finalize_kernel(const double* partial
     counts[0] = (first ? 0ull : counts[0]) + csum[0];
     counts[1] = (first ? 0ull : counts[1]) + csum[1];
   }
+}
+
+// ZGEMM-factored evaluation (the reference's production algorithm,
+// rooflab/gpp/kernel.py:98-114), valid when wx does not depend on the band:
+// W[ig, igp] = sum_band aqsntemp[ig, band] conj(aqsmtemp[igp, band]) comes
+// from one ZGEMM (cuBLAS, FP64 tensor cores); this kernel forms the branch
+// terms of variant V per (iw, ig, igp) exactly as the reference's
+// variant_terms does (PlainPolicy<V>, kernel.py:63-95) and contracts them with
+// W.  A different algorithm from the per-instance nest -- time to solution,
+// never a roofline figure.  Counts are scaled by nb, the
+// band count W summed over (kernel.py:130-137).
+template <int V, int NW>
+__global__ void __launch_bounds__(kThreads) gpp_factored_terms_kernel(
+    const double2* __restrict__ W, const double2* __restrict__ wtilde,
+    const double2* __restrict__ eps, const double* __restrict__ wx0, int nw_total, int iw0,
+    long long n_elems, unsigned long long nb, double* partials, unsigned long long* cpartials) {
+  Acc<NW> acc;
+#pragma unroll
+  for (int iw = 0; iw < NW; ++iw) {
+    acc.a[iw] = make_double2(0.0, 0.0);
+    acc.b[iw] = make_double2(0.0, 0.0);
+  }
+  acc.nn = 0;
+  acc.nf = 0;
+  double wx[NW];
+#pragma unroll
+  for (int iw = 0; iw < NW; ++iw) wx[iw] = __ldg(wx0 + iw0 + iw);
+  for (long long e = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x; e < n_elems;
+       e += static_cast<long long>(gridDim.x) * kThreads) {
+    const typename PlainPolicy<V>::St st = PlainPolicy<V>::make(__ldg(wtilde + e), __ldg(eps + e), true);
+    const double2 w = __ldg(W + e);
+    PlainPolicy<V>::template tuple<NW, true, false>(st, w.x, w.y, wx, acc);
+  }
+  block_reduce_write<NW, true>(acc, partials, cpartials, nb);
 }
 
 // FP64 pipe peak: 8 independent DFMA chains per thread, a = a * a + c.

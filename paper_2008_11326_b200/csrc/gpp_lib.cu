@@ -1,6 +1,7 @@
 // gpp_lib.cu -- host side of libgpp_b200.so: the C ABI declared in
 // include/gpp_b200.h, the device-buffer manager, launch planning, the NCCL
 // band-shard combine and the FP64 peak microbenchmark.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -111,6 +112,11 @@ struct gpp_ctx {
 
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+
+  // ZGEMM-factored path (gpp_run_factored).
+  bool wx_band_invariant = false;
+  cublasHandle_t blas = nullptr;
+  DevBuf<double2> weight;  // (ncouls, ngpown) F-order
 };
 
 namespace {
@@ -398,6 +404,8 @@ void gpp_destroy(gpp_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->cstream) cudaStreamSynchronize(c->cstream);
     if (c->comm) ncclCommDestroy(c->comm);
+    if (c->blas) cublasDestroy(c->blas);
+    c->weight.release();
     c->wtilde.release();
     c->eps.release();
     c->aqsn.release();
@@ -489,6 +497,10 @@ int prepare(gpp_ctx* c, const HostProblem& h) {
   }
   double wxmax = 0.0;
   for (size_t k = 0; k < n_wx; ++k) wxmax = std::max(wxmax, std::fabs(c->h_wx[k]));
+  bool invariant = true;
+  for (size_t k = static_cast<size_t>(h.nw); k < n_wx && invariant; ++k)
+    invariant = c->h_wx[k] == c->h_wx[k % h.nw];
+  c->wx_band_invariant = invariant;
   c->nbands = nb;
   c->ngpown = h.ngpown;
   c->ncouls = h.ncouls;
@@ -733,6 +745,78 @@ int gpp_comm_init(gpp_ctx* c, int nranks, int rank, const unsigned char* id128) 
   ncclUniqueId id;
   std::memcpy(&id, id128, sizeof(id));
   GPP_NCCL(ncclCommInitRank(&c->comm, nranks, id, rank));
+  return GPP_OK;
+}
+
+int gpp_run_factored(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp,
+                     int64_t* near_far, float* ms) {
+  if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
+  if (variant < GPP_VARIANT_DIV || variant > GPP_VARIANT_RCP_SQ)
+    return fail(GPP_ERR_ARG, "the factored path takes a reference variant (0=div, 1=rcp, 2=rcp_sq)");
+  if (!achtemp || !asxtemp) return fail(GPP_ERR_ARG, "output pointer is NULL");
+  if (!c->have_problem) return fail(GPP_ERR_ARG, "no problem uploaded");
+  if (!c->wx_band_invariant)
+    return fail(GPP_ERR_ARG, "the factored path needs a band-invariant wx (the reference's (nw,) vector)");
+  DeviceGuard g(c->device);
+  if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+  if (!c->blas) {
+    if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) return fail(GPP_ERR_CUDA, "cublasCreate failed");
+  }
+  if (cublasSetStream(c->blas, c->stream) != CUBLAS_STATUS_SUCCESS)
+    return fail(GPP_ERR_CUDA, "cublasSetStream failed");
+  const size_t n_el = static_cast<size_t>(c->ncouls) * c->ngpown;
+  GPP_CUDA(c->weight.ensure(n_el));
+  GPP_CUDA(cudaEventRecord(c->ev[2], c->stream));
+  // W = aqsn (nc x nb) * conj(aqsm)^T (nb x ng): one ZGEMM.
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+  const cublasStatus_t st = cublasZgemm(
+      c->blas, CUBLAS_OP_N, CUBLAS_OP_C, static_cast<int>(c->ncouls), static_cast<int>(c->ngpown),
+      static_cast<int>(c->nbands), &one, reinterpret_cast<const cuDoubleComplex*>(c->aqsn.ptr),
+      static_cast<int>(c->ncouls), reinterpret_cast<const cuDoubleComplex*>(c->aqsm.ptr),
+      static_cast<int>(c->ngpown), &zero, reinterpret_cast<cuDoubleComplex*>(c->weight.ptr),
+      static_cast<int>(c->ncouls));
+  if (st != CUBLAS_STATUS_SUCCESS) return fail(GPP_ERR_CUDA, "cublasZgemm failed");
+  std::vector<std::pair<int, int>> groups;
+  nw_groups(c->nw, &groups);
+  const int grid = std::max(1, std::min<int>(c->num_sms * 4, static_cast<int>(
+                                   (n_el + gpp::kThreads - 1) / gpp::kThreads)));
+  GPP_CUDA(c->partials.ensure(static_cast<size_t>(grid) * 4 * gpp::kMaxNwGroup));
+  GPP_CUDA(c->cpartials.ensure(static_cast<size_t>(grid) * 2));
+  bool first = true;
+  for (const auto& gr : groups) {
+    const int iw0 = gr.first, nwg = gr.second;
+#define GPP_FAC(V, NWC)                                                                          \
+  gpp::gpp_factored_terms_kernel<V, NWC><<<grid, gpp::kThreads, 0, c->stream>>>(                 \
+      c->weight.ptr, c->wtilde.ptr, c->eps.ptr, c->wxb.ptr, c->nw, iw0,                          \
+      static_cast<long long>(n_el), static_cast<unsigned long long>(c->nbands), c->partials.ptr, \
+      c->cpartials.ptr)
+#define GPP_FAC_NW(V)              \
+  switch (nwg) {                   \
+    case 1: GPP_FAC(V, 1); break;  \
+    case 2: GPP_FAC(V, 2); break;  \
+    case 3: GPP_FAC(V, 3); break;  \
+    default: GPP_FAC(V, 4); break; \
+  }
+    if (variant == GPP_VARIANT_DIV) {
+      GPP_FAC_NW(0)
+    } else if (variant == GPP_VARIANT_RCP) {
+      GPP_FAC_NW(1)
+    } else {
+      GPP_FAC_NW(2)
+    }
+#undef GPP_FAC_NW
+#undef GPP_FAC
+    GPP_CUDA(cudaGetLastError());
+    pick_finalize(nwg)<<<1, 256, 0, c->stream>>>(c->partials.ptr, c->cpartials.ptr, grid, c->nw,
+                                                  iw0, 0, first ? 1 : 0, 1, c->out.ptr,
+                                                  c->counts.ptr);
+    GPP_CUDA(cudaGetLastError());
+    first = false;
+  }
+  GPP_CUDA(cudaEventRecord(c->ev[3], c->stream));
+  int rc = finish_run(c, achtemp, asxtemp, near_far);
+  if (rc) return rc;
+  if (ms) GPP_CUDA(cudaEventElapsedTime(ms, c->ev[2], c->ev[3]));
   return GPP_OK;
 }
 

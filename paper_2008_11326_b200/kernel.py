@@ -195,6 +195,25 @@ class GPPContext:
                            asxtemp=asx.view(np.complex128).copy())
         return result, ((int(nf[0]), int(nf[1])) if counts else None), float(ms.value)
 
+    def run_factored(self, variant: str = "rcp_sq", counts: bool = True):
+        """The reference's ZGEMM-factored algorithm on the device
+        (gpp_run_factored): (GPPResult, (near, far) | None, device_ms).
+        Band-invariant wx only; a different algorithm from run()."""
+        _reference_variant(variant)
+        if self.nw < 1:
+            raise DomainError("no problem uploaded")
+        ach = np.empty(2 * self.nw, dtype=np.float64)
+        asx = np.empty(2 * self.nw, dtype=np.float64)
+        nf = np.zeros(2, dtype=np.int64)
+        ms = ctypes.c_float()
+        nf_ptr = nf.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)) if counts else None
+        _lib.check(self._lib.gpp_run_factored(self._h, _variant_code(variant), _lib.dptr(ach),
+                                              _lib.dptr(asx), nf_ptr, ctypes.byref(ms)),
+                   "gpp_run_factored")
+        result = GPPResult(achtemp=ach.view(np.complex128).copy(),
+                           asxtemp=asx.view(np.complex128).copy())
+        return result, ((int(nf[0]), int(nf[1])) if counts else None), float(ms.value)
+
     def time(self, variant: str = "rcp_sq", iters: int = 10) -> tuple[float, float]:
         """Device-resident timing of ``iters`` evaluations: (total_ms, main_kernel_ms)."""
         tot, main = ctypes.c_float(), ctypes.c_float()
@@ -264,6 +283,16 @@ def reference_result(problem, device: int = 0) -> GPPResult:
     """The literal-nest formulation (problem.py:179-208: library complex
     division and magnitude predicates) evaluated per instance on the GPU."""
     return evaluate(problem, "div", device, counts=False)[0]
+
+
+def evaluate_factored(problem, variant: str = "rcp_sq", device: int = 0) -> GPPResult:
+    """The reference's production algorithm (kernel.py:98-114: ZGEMM of the
+    band weights, then the branch terms) on the GPU.  Time-to-solution path
+    for band-invariant wx; evaluate_variant runs the per-instance nest."""
+    _reference_variant(variant)
+    ctx = get_context(device)
+    ctx.upload(problem)
+    return ctx.run_factored(variant, counts=False)[0]
 
 
 def fp64_peak(device: int = 0, iters: int = 200_000) -> tuple[float, float]:

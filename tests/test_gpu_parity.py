@@ -288,3 +288,32 @@ def test_single_process_group_api():
         g.close()
     with pytest.raises(ValueError):
         MultiDeviceGPP([0, 0])
+
+
+@pytest.mark.parametrize("variant", ["div", "rcp", "rcp_sq"])
+def test_factored_path_vs_reference(variant):
+    """gpp_run_factored (ZGEMM + terms, the reference's own algorithm)."""
+    ctx = GPPContext(0)
+    try:
+        for case in [c for c in SMALL if c["dims"] in ([5, 3, 40], [47, 2, 33], [64, 64, 512])]:
+            p = synth_problem(*case["dims"], seed=case["seed"], nw=case["nw"])
+            ctx.upload(p)
+            got, nf, ms = ctx.run_factored(variant, counts=True)
+            assert max_rel_error(got, _R(case["evaluate_variant"][variant])) <= 1e-12
+            assert [case["nw"] * int(np.prod(case["dims"])), *nf] == case["branch_stats"][variant]
+        case = next(c for c in BIG if c["dims"] == [512, 66, 32768] and c["seed"] == 1 and c["nw"] == 3)
+        p = synth_problem(512, 66, 32768, seed=1, nw=3, check=False)
+        ctx.upload(p)
+        got, nf, ms = ctx.run_factored(variant, counts=True)
+        assert max_rel_error(got, _R(case["evaluate_variant"]["rcp_sq"])) <= TOL
+        if variant == "rcp_sq":
+            assert [3 * 512 * 66 * 32768, *nf] == case["branch_stats"]["rcp_sq"]
+        # band-indexed wx with distinct columns is not factorable
+        wxb = np.asfortranarray(np.stack([p.wx] * 511 + [p.wx + 0.01], axis=1))
+        q = GPPProblem(512, 66, 32768, p.wtilde, p.i_eps, p.aqsntemp, p.aqsmtemp, wxb)
+        ctx.upload(q)
+        from paper_2008_11326_b200.errors import DomainError
+        with pytest.raises(DomainError):
+            ctx.run_factored(variant)
+    finally:
+        ctx.close()
