@@ -114,6 +114,16 @@ int gpp_upload(gpp_ctx* ctx, int64_t nbands, int64_t ngpown, int64_t ncouls, int
 int gpp_run(gpp_ctx* ctx, int32_t variant, double* achtemp, double* asxtemp,
             int64_t* near_far, float* kernel_ms);
 
+/* Synthesize the problem on the device instead of uploading it: the arrays
+ * synth_problem(nbands, ngpown, ncouls, seed, nw) draws (rooflab/gpp/
+ * problem.py:109-156, numpy PCG64 + Generator.uniform), bit-exact, for the
+ * band shard [band0, band1).  pcg_state = {state.lo, state.hi, inc.lo,
+ * inc.hi} of np.random.default_rng(seed) right after seeding; wx = the nw
+ * frequencies (drawn on the host, they are the last nw draws).  The
+ * branch-margin scan (problem.py:159-176) is not run. */
+int gpp_synth(gpp_ctx* ctx, int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw,
+              const uint64_t* pcg_state, const double* wx, int64_t band0, int64_t band1);
+
 /* Upload + evaluate in one call, with the host->device copy pipelined
  * against the computation: the ig rows of wtilde / i_eps / aqsntemp are
  * copied in `slabs` ig slabs (<= 0: 16) on a copy stream, and the kernel for

@@ -39,6 +39,11 @@ SIGNATURES = {
          _c_double_p, _c_double_p, _c_double_p, _c_double_p, _c_double_p, ctypes.c_int32,
          ctypes.c_int64, ctypes.c_int64],
     ),
+    "gpp_synth": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+         ctypes.POINTER(ctypes.c_uint64), _c_double_p, ctypes.c_int64, ctypes.c_int64],
+    ),
     "gpp_run": (
         ctypes.c_int,
         [ctypes.c_void_p, ctypes.c_int32, _c_double_p, _c_double_p, _c_i64_p, _c_float_p],

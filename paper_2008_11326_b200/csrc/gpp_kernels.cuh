@@ -712,6 +712,74 @@ __global__ void __launch_bounds__(kThreads) gpp_factored_terms_kernel(
   block_reduce_write<NW, true>(acc, partials, cpartials, nb);
 }
 
+// ---------------------------------------------------------------------------
+// Device-side synthesis: numpy's PCG64 (128-bit LCG, XSL-RR output) and
+// Generator.uniform, bit-exact with synth_problem (rooflab/gpp/problem.py:
+// 109-156).  The host passes the generator state after seeding; every thread
+// jumps to its first draw with the O(log n) LCG advance and then steps.
+// ---------------------------------------------------------------------------
+struct U128 {
+  unsigned long long lo, hi;
+};
+__device__ __forceinline__ U128 mul128(U128 a, U128 b) {
+  U128 r;
+  r.lo = a.lo * b.lo;
+  r.hi = __umul64hi(a.lo, b.lo) + a.lo * b.hi + a.hi * b.lo;
+  return r;
+}
+__device__ __forceinline__ U128 add128(U128 a, U128 b) {
+  U128 r;
+  r.lo = a.lo + b.lo;
+  r.hi = a.hi + b.hi + (r.lo < a.lo ? 1ull : 0ull);
+  return r;
+}
+constexpr unsigned long long kPcgMulHi = 0x2360ED051FC65DA4ull;
+constexpr unsigned long long kPcgMulLo = 0x4385DF649FCCF645ull;
+
+// state after `delta` further steps (pcg_advance_lcg_128).
+__device__ __forceinline__ U128 pcg_advance(U128 state, U128 inc, unsigned long long delta) {
+  U128 acc_mult{1ull, 0ull}, acc_plus{0ull, 0ull};
+  U128 cur_mult{kPcgMulLo, kPcgMulHi}, cur_plus = inc;
+  while (delta) {
+    if (delta & 1ull) {
+      acc_mult = mul128(acc_mult, cur_mult);
+      acc_plus = add128(mul128(acc_plus, cur_mult), cur_plus);
+    }
+    cur_plus = mul128(add128(cur_mult, U128{1ull, 0ull}), cur_plus);
+    cur_mult = mul128(cur_mult, cur_mult);
+    delta >>= 1;
+  }
+  return add128(mul128(acc_mult, state), acc_plus);
+}
+
+// One draw: step, XSL-RR output, 53-bit double in [0, 1).
+__device__ __forceinline__ double pcg_next_double(U128& state, U128 inc) {
+  state = add128(mul128(state, U128{kPcgMulLo, kPcgMulHi}), inc);
+  const unsigned long long x = state.hi ^ state.lo;
+  const unsigned rot = static_cast<unsigned>(state.hi >> 58);
+  const unsigned long long out = (x >> rot) | (x << ((64u - rot) & 63u));
+  return static_cast<double>(out >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// Fill one real or imaginary component of an F-order complex matrix whose
+// draws are laid out C-order over (rows, cols) starting at draw `offset`;
+// only columns [c0, c1) are produced, at dst[(i + (c - c0) * rows)].  Thread
+// i owns row i: one jump, then sequential steps along its row, so for a
+// fixed column the warp writes consecutive rows (coalesced).
+__global__ void __launch_bounds__(256) gpp_synth_kernel(U128 state0, U128 inc,
+                                                        unsigned long long offset, long long rows,
+                                                        long long cols, long long c0, long long c1,
+                                                        double* dst, int comp) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < rows;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    U128 s = pcg_advance(state0, inc, offset + static_cast<unsigned long long>(i * cols + c0));
+    for (long long c = c0; c < c1; ++c) {
+      const double u = pcg_next_double(s, inc);
+      dst[2 * (i + (c - c0) * rows) + comp] = fma(2.0, u, -1.0);  // uniform(-1, 1)
+    }
+  }
+}
+
 // FP64 pipe peak: 8 independent DFMA chains per thread, a = a * a + c.
 // One register operand per DFMA keeps the operand collector out of the way
 // (a DFMA with three distinct register operands runs at 2/3 rate on B200,

@@ -509,15 +509,21 @@ int prepare(gpp_ctx* c, const HostProblem& h) {
   return GPP_OK;
 }
 
+// H2D of the expanded wx (pinned staging) on stream s.
+int copy_small_wx(gpp_ctx* c, const HostProblem& h, cudaStream_t s) {
+  const int64_t nb = h.band1 - h.band0;
+  GPP_CUDA(cudaMemcpyAsync(c->wxb.ptr, c->h_wx, static_cast<size_t>(nb) * h.nw * sizeof(double),
+                           cudaMemcpyHostToDevice, s));
+  return GPP_OK;
+}
+
 // H2D of the small arrays (aqsmtemp shard, expanded wx) on stream s.
 int copy_small(gpp_ctx* c, const HostProblem& h, cudaStream_t s) {
   const int64_t nb = h.band1 - h.band0;
   GPP_CUDA(cudaMemcpyAsync(c->aqsm.ptr, h.aqsmtemp + 2 * static_cast<size_t>(h.band0) * h.ngpown,
                            static_cast<size_t>(h.ngpown) * nb * sizeof(double2),
                            cudaMemcpyHostToDevice, s));
-  GPP_CUDA(cudaMemcpyAsync(c->wxb.ptr, c->h_wx, static_cast<size_t>(nb) * h.nw * sizeof(double),
-                           cudaMemcpyHostToDevice, s));
-  return GPP_OK;
+  return copy_small_wx(c, h, s);
 }
 
 // H2D of the ig rows [i0, i1) of wtilde, i_eps and the aqsntemp shard:
@@ -745,6 +751,59 @@ int gpp_comm_init(gpp_ctx* c, int nranks, int rank, const unsigned char* id128) 
   ncclUniqueId id;
   std::memcpy(&id, id128, sizeof(id));
   GPP_NCCL(ncclCommInitRank(&c->comm, nranks, id, rank));
+  return GPP_OK;
+}
+
+int gpp_synth(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw,
+              const uint64_t* pcg_state, const double* wx, int64_t band0, int64_t band1) {
+  if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
+  if (!pcg_state || !wx) return fail(GPP_ERR_ARG, "pcg_state / wx is NULL");
+  // Validate like an upload (the array pointers are not used).
+  const double dummy = 0.0;
+  const HostProblem h{nbands, ngpown, ncouls, nw, &dummy, &dummy, &dummy, &dummy, wx, 0,
+                      band0, band1};
+  int rc = validate(c, h);
+  if (rc) return rc;
+  rc = ensure_init(c);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
+  if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+  c->have_problem = false;
+  rc = prepare(c, h);
+  if (rc) return rc;
+  const gpp::U128 st{pcg_state[0], pcg_state[1]}, inc{pcg_state[2], pcg_state[3]};
+  const unsigned long long nwt = static_cast<unsigned long long>(ncouls) * ngpown;
+  const unsigned long long nan_ = static_cast<unsigned long long>(ncouls) * nbands;
+  // Draw order of synth_problem (problem.py:136-141): wtilde re, im; i_eps re,
+  // im; aqsntemp re, im; aqsmtemp re, im; then wx.
+  struct Block {
+    unsigned long long offset;
+    long long rows, cols, c0, c1;
+    double2* dst;
+    int comp;
+  };
+  const Block blocks[8] = {
+      {0, ncouls, ngpown, 0, ngpown, c->wtilde.ptr, 0},
+      {nwt, ncouls, ngpown, 0, ngpown, c->wtilde.ptr, 1},
+      {2 * nwt, ncouls, ngpown, 0, ngpown, c->eps.ptr, 0},
+      {3 * nwt, ncouls, ngpown, 0, ngpown, c->eps.ptr, 1},
+      {4 * nwt, ncouls, nbands, band0, band1, c->aqsn.ptr, 0},
+      {4 * nwt + nan_, ncouls, nbands, band0, band1, c->aqsn.ptr, 1},
+      {4 * nwt + 2 * nan_, ngpown, nbands, band0, band1, c->aqsm.ptr, 0},
+      {4 * nwt + 2 * nan_ + static_cast<unsigned long long>(ngpown) * nbands, ngpown, nbands,
+       band0, band1, c->aqsm.ptr, 1},
+  };
+  for (const Block& b : blocks) {
+    const int grid = static_cast<int>(std::min<long long>((b.rows + 255) / 256, 65535));
+    gpp::gpp_synth_kernel<<<grid, 256, 0, c->stream>>>(st, inc, b.offset, b.rows, b.cols, b.c0,
+                                                       b.c1, reinterpret_cast<double*>(b.dst),
+                                                       b.comp);
+    GPP_CUDA(cudaGetLastError());
+  }
+  rc = copy_small_wx(c, h, c->stream);
+  if (rc) return rc;
+  GPP_CUDA(cudaStreamSynchronize(c->stream));
+  c->have_problem = true;
   return GPP_OK;
 }
 

@@ -172,6 +172,36 @@ class GPPContext:
                            asxtemp=asx.view(np.complex128).copy())
         return result, ((int(nf[0]), int(nf[1])) if counts else None), float(ms.value)
 
+    def synth(self, nbands: int, ngpown: int, ncouls: int, seed: int = 42, nw: int = 2,
+              band_range: tuple[int, int] | None = None) -> None:
+        """Draw synth_problem(nbands, ngpown, ncouls, seed, nw) directly on
+        the device (gpp_synth, bit-exact with the host draw; no H2D of the
+        arrays).  The device then holds the problem (or its band shard)."""
+        from .problem import MAX_NW
+
+        for name, value in (("nbands", nbands), ("ngpown", ngpown), ("ncouls", ncouls)):
+            if value < 1:
+                raise DomainError(f"{name} must be at least 1, got {value!r}")
+        if not 1 <= nw <= MAX_NW:
+            raise DomainError(f"nw must be in [1, {MAX_NW}], got {nw!r}")
+        b0, b1 = (0, nbands) if band_range is None else (int(band_range[0]), int(band_range[1]))
+        rng = np.random.default_rng(seed)
+        st = rng.bit_generator.state["state"]
+        mask = (1 << 64) - 1
+        words = np.array([st["state"] & mask, st["state"] >> 64, st["inc"] & mask, st["inc"] >> 64],
+                         dtype=np.uint64)
+        # wx is drawn last (problem.py:141): skip the 4 nc ng + 2 nc nb + 2 ng nb array draws.
+        rng.bit_generator.advance(4 * ncouls * ngpown + 2 * ncouls * nbands + 2 * ngpown * nbands)
+        wx = rng.uniform(1.0, 2.0, size=nw)
+        self._key = None
+        _lib.check(self._lib.gpp_synth(self._h, int(nbands), int(ngpown), int(ncouls), int(nw),
+                                       words.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                       _lib.dptr(wx), b0, b1), "gpp_synth")
+        self.nw = int(nw)
+        self.band_range = (b0, b1)
+        self.dims = (int(nbands), int(ngpown), int(ncouls))
+        self.synth_wx = wx
+
     def run(self, variant: str = "rcp_sq", counts: bool = True):
         """Evaluate the uploaded problem: (GPPResult, (near, far) | None, kernel_ms).
 

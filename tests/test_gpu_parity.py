@@ -317,3 +317,27 @@ def test_factored_path_vs_reference(variant):
             ctx.run_factored(variant)
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("dims,seed,nw,br", [
+    ((5, 3, 40), 1, 2, None), ((47, 2, 33), 7, 3, None), ((64, 64, 512), 42, 2, (10, 50)),
+    ((512, 66, 32768), 1, 3, None),
+])
+def test_device_synthesis_is_bitexact(dims, seed, nw, br):
+    """gpp_synth draws synth_problem's arrays on the device (numpy PCG64 +
+    uniform, bit-exact): the kernel sees identical inputs, so its result is
+    bitwise the host-synthesized one."""
+    p = synth_problem(*dims, seed=seed, nw=nw, check=False)
+    a = GPPContext(0)
+    b = GPPContext(0)
+    try:
+        a.synth(*dims, seed=seed, nw=nw, band_range=br)
+        assert np.array_equal(a.synth_wx, p.wx)
+        b.upload(p, br)
+        ra, nfa, _ = a.run("rcp_sq", counts=True)
+        rb, nfb, _ = b.run("rcp_sq", counts=True)
+        assert nfa == nfb
+        assert np.array_equal(ra.achtemp, rb.achtemp) and np.array_equal(ra.asxtemp, rb.asxtemp)
+    finally:
+        a.close()
+        b.close()
