@@ -11,7 +11,19 @@ if str(ROOT) not in sys.path:
 GOLDEN = ROOT / "tests" / "golden"
 
 
+def _ensure_library() -> None:
+    """Build libgpp_b200.so in-tree if it is missing (nvcc cross-compiles for
+    sm_100a without a GPU), so the suite runs from a clean checkout."""
+    lib = ROOT / "paper_2008_11326_b200" / "lib" / "libgpp_b200.so"
+    if not lib.exists():
+        import subprocess
+
+        subprocess.run(["make", "-C", str(ROOT / "paper_2008_11326_b200" / "csrc")], check=True,
+                       stdout=subprocess.DEVNULL)
+
+
 def pytest_configure(config):
+    _ensure_library()
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built library")
     config.addinivalue_line("markers", "slow: long-running (large problem sizes)")
 
