@@ -177,33 +177,38 @@ def _igp_slice(problem, g0: int, g1: int):
                       problem.aqsntemp, np.asfortranarray(problem.aqsmtemp[g0:g1, :]), problem.wx)
 
 
-def cpu_reference_steps(problem, steps: int, warmup: int, igp_per_step: int):
-    """Time the reference's production CPU path (evaluate_variant, the ZGEMM-
+class CpuReference:
+    """The reference's production CPU path (evaluate_variant, the ZGEMM-
     factored numpy code, restated in oracle/gpp_oracle.py) on igp slices of
     the workload: every step evaluates `igp_per_step` igp columns of the full
-    problem, rotating through all of them.  Returns (flops, seconds) of the
-    timed steps; FLOPs are the reference's analytic count of each slice."""
-    from oracle import gpp_oracle as orc
-    from paper_2008_11326_b200.counters import algorithmic_flops
+    problem, rotating through all of them.  FLOPs of a step are the
+    reference's analytic count of its slice (computed once, untimed)."""
 
-    ng = problem.ngpown
-    slices = [(g, min(g + igp_per_step, ng)) for g in range(0, ng, igp_per_step)]
-    subs = [_igp_slice(problem, a, b) for a, b in slices]
-    fl = []
-    for s in subs:
-        _, near, far = orc.branch_stats(s, "rcp_sq")
-        fl.append(algorithmic_flops(s.nbands, s.ngpown, s.ncouls, len(s.wx), near, far))
-    for i in range(warmup):
-        orc.evaluate_variant(subs[i % len(subs)], "rcp_sq")
-    flops = 0
-    secs = 0.0
-    for i in range(steps):
-        k = i % len(subs)
-        t0 = time.perf_counter()
-        orc.evaluate_variant(subs[k], "rcp_sq")
-        secs += time.perf_counter() - t0
-        flops += fl[k]
-    return flops, secs
+    def __init__(self, problem, igp_per_step: int):
+        from oracle import gpp_oracle as orc
+        from paper_2008_11326_b200.counters import algorithmic_flops
+
+        self.orc = orc
+        ng = problem.ngpown
+        slices = [(g, min(g + igp_per_step, ng)) for g in range(0, ng, igp_per_step)]
+        self.subs = [_igp_slice(problem, a, b) for a, b in slices]
+        self.flops = []
+        for sub in self.subs:
+            _, near, far = orc.branch_stats(sub, "rcp_sq")
+            self.flops.append(algorithmic_flops(sub.nbands, sub.ngpown, sub.ncouls, len(sub.wx), near, far))
+
+    def run(self, steps: int, warmup: int = 0):
+        """(flops, seconds) of `steps` timed slice evaluations."""
+        for i in range(warmup):
+            self.orc.evaluate_variant(self.subs[i % len(self.subs)], "rcp_sq")
+        flops, secs = 0, 0.0
+        for i in range(steps):
+            k = i % len(self.subs)
+            t0 = time.perf_counter()
+            self.orc.evaluate_variant(self.subs[k], "rcp_sq")
+            secs += time.perf_counter() - t0
+            flops += self.flops[k]
+        return flops, secs
 
 
 # ----------------------------------------------------------------------------
@@ -243,7 +248,7 @@ def run_reference(args, dist: Dist):
     dims = WORKLOADS[args.workload]
     p = synth_problem(*dims, seed=args.seed, nw=args.nw, check=False)
     igp_per_step = 6
-    flops, secs = cpu_reference_steps(p, args.steps, args.warmup, igp_per_step)
+    flops, secs = CpuReference(p, igp_per_step).run(args.steps, args.warmup)
     value = flops / secs / 1e12
     cores = _cpu_threads()
     sample = (f"each step = reference evaluate_variant('rcp_sq') (ZGEMM-factored numpy, "
@@ -300,15 +305,23 @@ def run_ours(args, dist: Dist):
 
     # ---- device-resident timed region -----------------------------------
     ctx.time(args.variant, args.warmup)
-    dist.barrier()
-    dist.sync()
-    clocks = Clocks(list(range(dist.world)) if dist.rank == 0 else [])
-    if dist.rank == 0:
-        clocks.start()
-    total_ms, main_ms = ctx.time(args.variant, args.steps)
-    dist.sync()
-    dist.barrier()
-    clk = clocks.stop() if dist.rank == 0 else None
+    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    for attempt in range(2):  # a run that saw a slowdown reason is re-measured once
+        dist.barrier()
+        dist.sync()
+        clocks = Clocks(list(range(dist.world)) if dist.rank == 0 else [])
+        if dist.rank == 0:
+            clocks.start()
+        total_ms, main_ms = ctx.time(args.variant, args.steps)
+        dist.sync()
+        dist.barrier()
+        clk = clocks.stop() if dist.rank == 0 else None
+        retry = 1.0 if (clk and bad & set(clk.get("reasons", []))) else 0.0
+        if attempt == 0 and dist.max(retry) > 0:
+            continue
+        if clk is not None:
+            clk["remeasured"] = attempt > 0
+        break
     t_step_ms = dist.max(total_ms) / args.steps
     t_main_ms = dist.max(main_ms) / args.steps
     value = flops_job / (t_step_ms * 1e-3) / 1e12
@@ -368,13 +381,19 @@ def run_ours(args, dist: Dist):
     # ---- CPU baseline (rank 0, N=1 only) ---------------------------------
     cpu = None
     if dist.world == 1 and not args.no_cpu_baseline:
+        # Whole passes over the workload until >= 10 s of CPU work (at most
+        # 20 passes); the rate is total algorithmic FLOPs / total time.
         igp_per_step = 6
         steps = -(-ng // igp_per_step)  # one full pass over the workload
-        fl, secs = cpu_reference_steps(p, steps, 1, igp_per_step)
-        cpu = {"value": fl / secs / 1e12, "unit": "TFLOP/s", "cores": _cpu_threads(), "kind": "port",
-               "sample": f"one full pass of the {dims} nw={args.nw} workload through the reference's "
-                         f"evaluate_variant('rcp_sq') restated in oracle/ (numpy + OpenBLAS ZGEMM), "
-                         f"in {steps} igp slices of {igp_per_step}; {secs:.2f} s",
+        cref = CpuReference(p, igp_per_step)
+        fl_tot, secs_tot, passes = 0, 0.0, 0
+        while passes < 20 and (secs_tot < 10.0 or passes < 1):
+            fl, secs = cref.run(steps, 1 if passes == 0 else 0)
+            fl_tot, secs_tot, passes = fl_tot + fl, secs_tot + secs, passes + 1
+        cpu = {"value": fl_tot / secs_tot / 1e12, "unit": "TFLOP/s", "cores": _cpu_threads(), "kind": "port",
+               "sample": f"{passes} full passes of the {dims} nw={args.nw} workload through the "
+                         f"reference's evaluate_variant('rcp_sq') restated in oracle/ (numpy + OpenBLAS "
+                         f"ZGEMM), each in {steps} igp slices of {igp_per_step}; {secs_tot:.1f} s",
                "cpu_count": os.cpu_count()}
 
     prof = load_profile_summary() or {}
