@@ -113,6 +113,10 @@ struct gpp_ctx {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
 
+  // Launch plans of the uploaded problem, keyed by (variant, nw group, count);
+  // cleared whenever a problem is (re)loaded.
+  std::vector<std::pair<int, std::vector<int64_t>>> plan_cache;
+
   // ZGEMM-factored path (gpp_run_factored).
   bool wx_band_invariant = false;
   cublasHandle_t blas = nullptr;
@@ -245,7 +249,7 @@ int choose_igp_tile(int64_t ngpown) {
   return cost4 < cost3 ? 4 : 3;
 }
 
-int make_plan(gpp_ctx* c, int variant, int nw_group, bool count, Plan* pl) {
+int make_plan_uncached(gpp_ctx* c, int variant, int nw_group, bool count, Plan* pl) {
   // The plain (as-written) variants keep two igp per thread and the fast
   // kernel drops to 3 at four frequencies: both choices avoid spills under
   // the 128-register budget of __launch_bounds__(256, 2).
@@ -279,6 +283,32 @@ int make_plan(gpp_ctx* c, int variant, int nw_group, bool count, Plan* pl) {
   return GPP_OK;
 }
 
+// make_plan_uncached, memoised per context: the occupancy / attribute queries
+// cost host time that would otherwise dominate small problems.
+int make_plan(gpp_ctx* c, int variant, int nw_group, bool count, Plan* pl) {
+  const int key = (variant * 16 + nw_group) * 2 + (count ? 1 : 0);
+  for (const auto& e : c->plan_cache) {
+    if (e.first == key) {
+      const std::vector<int64_t>& v = e.second;
+      pl->igp_t = static_cast<int>(v[0]);
+      pl->bchunk = static_cast<int>(v[1]);
+      pl->n_igblk = static_cast<int>(v[2]);
+      pl->n_igptile = static_cast<int>(v[3]);
+      pl->n_items = v[4];
+      pl->grid = static_cast<int>(v[5]);
+      pl->blocks_per_sm = static_cast<int>(v[6]);
+      pl->regs = static_cast<int>(v[7]);
+      return GPP_OK;
+    }
+  }
+  int rc = make_plan_uncached(c, variant, nw_group, count, pl);
+  if (rc) return rc;
+  c->plan_cache.emplace_back(key, std::vector<int64_t>{pl->igp_t, pl->bchunk, pl->n_igblk,
+                                                       pl->n_igptile, pl->n_items, pl->grid,
+                                                       pl->blocks_per_sm, pl->regs});
+  return GPP_OK;
+}
+
 int nw_groups(int nw, std::vector<std::pair<int, int>>* groups) {
   groups->clear();
   for (int iw0 = 0; iw0 < nw; iw0 += gpp::kMaxNwGroup)
@@ -286,8 +316,6 @@ int nw_groups(int nw, std::vector<std::pair<int, int>>* groups) {
   return GPP_OK;
 }
 
-// Enqueue one full evaluation on c->stream.  If ev_main is non-null, the
-// main kernels of all frequency groups are bracketed by ev_main[0..1].
 // Optional ig-slab schedule of one evaluation: slab s covers the 256-ig blocks
 // [blk0[s], blk0[s+1]) and its launch waits on ready[s] (the H2D of its rows).
 struct SlabSched {
@@ -501,6 +529,7 @@ int prepare(gpp_ctx* c, const HostProblem& h) {
   for (size_t k = static_cast<size_t>(h.nw); k < n_wx && invariant; ++k)
     invariant = c->h_wx[k] == c->h_wx[k % h.nw];
   c->wx_band_invariant = invariant;
+  c->plan_cache.clear();
   c->nbands = nb;
   c->ngpown = h.ngpown;
   c->ncouls = h.ncouls;

@@ -11,12 +11,24 @@ from oracle import gpp_oracle as orc
 from paper_2008_11326_b200 import GPPContext, GPPProblem, synth_problem
 from paper_2008_11326_b200.dist import shard_problem
 from paper_2008_11326_b200.errors import SynthesisError
-from paper_2008_11326_b200.problem import max_rel_error
 
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-10
 _CTX = {}
+
+
+def _err(got, want) -> float:
+    """max_rel_error, except that components the reference has exactly zero
+    (possible for tiny random problems, e.g. no near instance at some iw) are
+    compared absolutely against the accumulators' scale."""
+    worst = 0.0
+    for g, w in ((got.achtemp, want.achtemp), (got.asxtemp, want.asxtemp)):
+        g, w = np.asarray(g), np.asarray(w)
+        scale = max(float(np.max(np.abs(w))), 1e-300)
+        denom = np.where(np.abs(w) > 0, np.abs(w), scale)
+        worst = max(worst, float(np.max(np.abs(g - w) / denom)))
+    return worst
 
 
 def _ctx():
@@ -58,9 +70,9 @@ def test_random_problems(case):
     ctx = _ctx()
     ctx.upload(p, force=True)
     got, nf, _ = ctx.run(kernel, counts=True)
-    assert max_rel_error(got, whole) <= TOL
+    assert _err(got, whole) <= TOL
     fast, _, _ = ctx.run(kernel, counts=False)
-    assert max_rel_error(fast, whole) <= TOL
+    assert _err(fast, whole) <= TOL
     part, nfs, _ = ctx.evaluate_host(p, kernel, band_range=br, counts=True, slabs=3)
-    assert max_rel_error(part, want_shard) <= TOL
+    assert _err(part, want_shard) <= TOL
     assert nfs == (near, far)
