@@ -59,7 +59,7 @@ def problems(draw):
     return p, (b0, b1), kernel
 
 
-@settings(max_examples=150, deadline=None, suppress_health_check=list(HealthCheck))
+@settings(max_examples=150, deadline=None, derandomize=True, suppress_health_check=list(HealthCheck))
 @given(problems())
 def test_random_problems(case):
     p, br, kernel = case
