@@ -199,7 +199,6 @@ struct FastPolicyT {
   struct St {
     double wtr, wti, wti2, wt2, qn, iwt2, er, ei;
   };
-  static constexpr bool kFast = true;
   static constexpr bool kHasFastPath = false;
   __device__ __forceinline__ static bool regular(const St&, double) { return false; }
 
@@ -277,7 +276,6 @@ struct FastPolicy3 {
   struct St {
     double wtr, wti, wti2, wt2, qn, rwt, er, ei;
   };
-  static constexpr bool kFast = true;
   static constexpr bool kHasFastPath = true;
 
   __device__ __forceinline__ static St make(double2 wt, double2 e, bool valid) {
@@ -378,7 +376,6 @@ struct PlainPolicy {
     double wtr, wti, er, ei;
     bool valid;
   };
-  static constexpr bool kFast = false;
   static constexpr bool kHasFastPath = false;
 
   __device__ __forceinline__ static St make(double2 wt, double2 e, bool valid) {
@@ -546,8 +543,8 @@ __device__ __forceinline__ void band_loop(const double2* anp, int ncouls, int nb
   cp_async_wait<0>();
 }
 
-template <class P, int NW, int IGP_T, bool COUNT, int MINB = 2>
-__global__ void __launch_bounds__(kThreads, MINB) gpp_main_kernel(const Params p) {
+template <class P, int NW, int IGP_T, bool COUNT>
+__global__ void __launch_bounds__(kThreads, 2) gpp_main_kernel(const Params p) {
   __shared__ double2 s_am[kMaxChunk][IGP_T];
   __shared__ double s_wx[kMaxChunk][NW];
   __shared__ __align__(16) double2 s_an[kAnDepth][kThreads];

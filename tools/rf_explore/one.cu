@@ -9,4 +9,4 @@
 #ifndef IGPV
 #define IGPV 3
 #endif
-template __global__ void gpp::gpp_main_kernel<POLICY, NWV, IGPV, false, 2>(gpp::Params);
+template __global__ void gpp::gpp_main_kernel<POLICY, NWV, IGPV, false>(gpp::Params);
