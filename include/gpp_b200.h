@@ -62,11 +62,14 @@ extern "C" {
  *   SQ_SPLIT  squared-magnitude predicates as integer compares, separate
  *             MUFU seeds for 1/d and sqrt, per-instance y    (paper v3-v4)
  *   IW_HOIST  eps*t, wt*(eps*t), |wt|^2 (eps*t) formed once per (band, igp,
- *             ig) and reused across frequencies              (paper v5-v7)
- * GPP_VARIANT_RCP_SQ is the final kernel (single rsqrt seed for 1/d and
- * sqrt(d), regular-item fast path; paper v8). */
+ *             ig) and reused across frequencies              (paper v5-v6)
+ *   ONE_SEED  one rsqrt seed for 1/d and sqrt(d), regular-item fast path
+ *             (far == !near)                                  (paper v7)
+ * GPP_VARIANT_RCP_SQ is the final kernel: per-(igp, iw) band sums, the
+ * (ig, igp) constants applied once per item (paper v8). */
 #define GPP_KERNEL_SQ_SPLIT 3
 #define GPP_KERNEL_IW_HOIST 4
+#define GPP_KERNEL_ONE_SEED 5
 
 typedef struct gpp_ctx gpp_ctx;
 

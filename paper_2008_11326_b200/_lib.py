@@ -19,7 +19,7 @@ LIB_PATH = Path(__file__).resolve().parent / "lib" / "libgpp_b200.so"
 GPP_OK, GPP_ERR_ARG, GPP_ERR_CUDA, GPP_ERR_NCCL, GPP_ERR_OOM = 0, 1, 2, 3, 4
 VARIANT_CODES = {"div": 0, "rcp": 1, "rcp_sq": 2}
 # Intermediate rcp_sq kernels of the version ladder (include/gpp_b200.h).
-KERNEL_CODES = {**VARIANT_CODES, "rcp_sq/split": 3, "rcp_sq/iw": 4}
+KERNEL_CODES = {**VARIANT_CODES, "rcp_sq/split": 3, "rcp_sq/iw": 4, "rcp_sq/seed": 5}
 
 _c_double_p = ctypes.POINTER(ctypes.c_double)
 _c_i64_p = ctypes.POINTER(ctypes.c_int64)

@@ -610,6 +610,215 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_main_kernel(const Params p) {
   block_reduce_write<NW, COUNT>(acc, p.partials, p.cpartials, 1ull);
 }
 
+// ---------------------------------------------------------------------------
+// Production kernel: per-(igp, iw) band sums with the (ig, igp) constants
+// applied once per item.
+//
+// For one (ig, igp) the near term of every instance is
+//     inv (wx wt - |wt|^2) eps t = (eps wt) [inv wx t] - (eps |wt|^2) [inv t]
+// and the far term sqrt(d/|wt|^2) eps t = (eps / |wt|) [sqrt(d) t], where
+// only the bracketed factors change with the band.  The band loop therefore
+// accumulates, per igp of the tile and per frequency,
+//     S1 += (inv wx) t,   S2 += inv t,   Sf += sqrt(d) t
+// and the item epilogue multiplies by eps wt, eps |wt|^2 and eps / |wt|.
+// Every instance still evaluates its own d, 1/d, sqrt(d), branch decision and
+// accumulation (nothing is hoisted across bands; wx may depend on the band).
+// Against FastPolicy3 this drops eps*t, wt*(eps t), |wt|^2 (eps t) and
+// |wt|^-1 (eps t) from every (band, igp, ig) tuple: 9 % fewer register-file
+// reads per instance at nw = 3 and 21 % at nw = 2 (tools/sass_rf.py).  The
+// per-thread ach/asx accumulators live in shared memory (updated once per
+// item) to leave the registers to the S sums.
+// ---------------------------------------------------------------------------
+template <int NW, int IGP_T, bool COUNT, bool FAST>
+__device__ __forceinline__ void sacc_band_loop(const double2* anp, int ncouls, int nb,
+                                               double2 (&s_an)[kAnDepth][kThreads],
+                                               const double2 (&s_am)[kMaxChunk][IGP_T],
+                                               const double (&s_wx)[kMaxChunk][NW],
+                                               const double (&wtr)[IGP_T],
+                                               const double (&wti2)[IGP_T],
+                                               const double (&qn)[IGP_T],
+                                               double2 (&S1)[IGP_T][NW], double2 (&S2)[IGP_T][NW],
+                                               double2 (&Sf)[IGP_T][NW], Acc<1>& cnt) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int s = 0; s < kAnDepth - 1; ++s) {
+    if (s < nb) cp_async16(&s_an[s][tid], anp + static_cast<size_t>(s) * ncouls);
+    cp_async_commit();
+  }
+  for (int bb = 0; bb < nb; ++bb) {
+    const int pf = bb + kAnDepth - 1;
+    if (pf < nb) cp_async16(&s_an[pf % kAnDepth][tid], anp + static_cast<size_t>(pf) * ncouls);
+    cp_async_commit();
+    cp_async_wait<kAnDepth - 1>();
+    const double2 an = s_an[bb % kAnDepth][tid];
+    double wx[NW];
+#pragma unroll
+    for (int iw = 0; iw < NW; ++iw) wx[iw] = s_wx[bb][iw];
+#pragma unroll
+    for (int j = 0; j < IGP_T; ++j) {
+      const double2 am = s_am[bb][j];
+      const double tr = fma(an.x, am.x, an.y * am.y);  // t = an * conj(am)
+      const double ti = fma(an.y, am.x, -an.x * am.y);
+      const long long qbits = __double_as_longlong(qn[j]);
+      double iwt2 = 0.0;
+      if constexpr (!FAST) {
+        // Padded lanes (qn = +inf) and wt = 0 get x = 0: never far.
+        const double wt2 = fma(wtr[j], wtr[j], wti2[j]);
+        iwt2 = (wt2 > 0.0 && qbits != 0x7FF0000000000000ll) ? 1.0 / wt2 : 0.0;
+      }
+#pragma unroll
+      for (int iw = 0; iw < NW; ++iw) {
+        const double wdre = wx[iw] - wtr[j];
+        const double d = fma(wdre, wdre, wti2[j]);
+        double in, gf;
+        if constexpr (FAST && !COUNT) {
+          // One rsqrt seed, one cubic step: 1/d = rr^2, sqrt(d) = t (1 + q).
+          const double r = rsqrt_approx(d);
+          const double t = d * r;
+          const double e = fma(-t, r, 1.0);
+          const double pe = fma(e, 0.375, 0.5);
+          const double q = e * pe;
+          const double rr = fma(r, q, r);
+          const double sq = fma(t, q, t);
+          const double inv = rr * rr;
+          asm("{\n\t.reg .pred pn;\n\t"
+              "setp.gt.s64 pn, %2, %3;\n\t"
+              "selp.f64 %0, %4, 0d0000000000000000, pn;\n\t"
+              "selp.f64 %1, 0d0000000000000000, %5, pn;\n\t}"
+              : "=d"(in), "=d"(gf)
+              : "l"(__double_as_longlong(d)), "l"(qbits), "d"(inv), "d"(sq));
+        } else {
+          // General path: full far test on x = d/|wt|^2; gf = sqrt(x)
+          // already carries the 1/|wt| factor.
+          const double inv = rcp_refined(d);
+          const double x = d * iwt2;
+          const double g = sqrt_nr<3>(x);
+          select_branches<COUNT>(d, qbits, x, inv, g, in, gf, cnt);
+        }
+        const double s1 = in * wx[iw];
+        S1[j][iw].x = fma(s1, tr, S1[j][iw].x);
+        S1[j][iw].y = fma(s1, ti, S1[j][iw].y);
+        S2[j][iw].x = fma(in, tr, S2[j][iw].x);
+        S2[j][iw].y = fma(in, ti, S2[j][iw].y);
+        Sf[j][iw].x = fma(gf, tr, Sf[j][iw].x);
+        Sf[j][iw].y = fma(gf, ti, Sf[j][iw].y);
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
+template <int NW, int IGP_T, bool COUNT>
+__global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const Params p) {
+  __shared__ double2 s_am[kMaxChunk][IGP_T];
+  __shared__ double s_wx[kMaxChunk][NW];
+  __shared__ __align__(16) double2 s_an[kAnDepth][kThreads];
+  __shared__ double s_acc[4 * NW][kThreads];  // this thread's ach/asx partials
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < 4 * NW; ++k) s_acc[k][tid] = 0.0;
+  Acc<1> cnt;
+  cnt.nn = 0;
+  cnt.nf = 0;
+
+  for (long long item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+    const int igpt = static_cast<int>(item % p.n_igptile);
+    const long long rest = item / p.n_igptile;
+    const int igb = static_cast<int>(rest % p.n_igblk);
+    const int bc = static_cast<int>(rest / p.n_igblk);
+    const int ig = (p.igblk0 + igb) * kThreads + tid;
+    const bool vig = ig < p.ncouls;
+    const int igc = vig ? ig : p.ncouls - 1;
+    const int b0 = bc * p.bchunk;
+    const int nb = min(p.bchunk, p.nbands - b0);
+
+    double wtr[IGP_T], wti2[IGP_T], qn[IGP_T];
+    bool thread_regular = true;
+#pragma unroll
+    for (int j = 0; j < IGP_T; ++j) {
+      const int igp = igpt * IGP_T + j;
+      const bool v = vig && igp < p.ngpown;
+      const size_t off = static_cast<size_t>(min(igp, p.ngpown - 1)) * p.ncouls + igc;
+      const double2 wt = __ldg(p.wtilde + off);
+      wtr[j] = wt.x;
+      wti2[j] = wt.y * wt.y;
+      const double wt2 = fma(wt.x, wt.x, wti2[j]);
+      qn[j] = v ? fmax(0.25, 0.25 * wt2) : __longlong_as_double(0x7FF0000000000000ll);
+      // Regular (see FastPolicy3::regular): no instance can be degenerate.
+      const double m = p.wxmax + sqrt(wt2);
+      thread_regular = thread_regular && (!v || (wt.y != 0.0 && wt2 > 1.000001e-24 * m * m));
+    }
+    const bool item_regular = __syncthreads_and(!COUNT && thread_regular) != 0;
+    for (int k = tid; k < nb * IGP_T; k += kThreads) {
+      const int bb = k / IGP_T, j = k - bb * IGP_T;
+      const int igp = igpt * IGP_T + j;
+      s_am[bb][j] = igp < p.ngpown
+                        ? __ldg(p.aqsm + static_cast<size_t>(b0 + bb) * p.ngpown + igp)
+                        : make_double2(0.0, 0.0);
+    }
+    for (int k = tid; k < nb * NW; k += kThreads) {
+      const int bb = k / NW, iw = k - bb * NW;
+      s_wx[bb][iw] = __ldg(p.wxb + static_cast<size_t>(b0 + bb) * p.nw_total + p.iw0 + iw);
+    }
+    __syncthreads();
+
+    double2 S1[IGP_T][NW], S2[IGP_T][NW], Sf[IGP_T][NW];
+#pragma unroll
+    for (int j = 0; j < IGP_T; ++j)
+#pragma unroll
+      for (int iw = 0; iw < NW; ++iw) {
+        S1[j][iw] = make_double2(0.0, 0.0);
+        S2[j][iw] = make_double2(0.0, 0.0);
+        Sf[j][iw] = make_double2(0.0, 0.0);
+      }
+    const double2* anp = p.aqsn + static_cast<size_t>(b0) * p.ncouls + igc;
+    if (item_regular)
+      sacc_band_loop<NW, IGP_T, COUNT, true>(anp, p.ncouls, nb, s_an, s_am, s_wx, wtr, wti2, qn,
+                                             S1, S2, Sf, cnt);
+    else
+      sacc_band_loop<NW, IGP_T, COUNT, false>(anp, p.ncouls, nb, s_an, s_am, s_wx, wtr, wti2, qn,
+                                              S1, S2, Sf, cnt);
+
+    // Item epilogue: apply the (ig, igp) constants once.
+    double a[4 * NW];
+#pragma unroll
+    for (int k = 0; k < 4 * NW; ++k) a[k] = s_acc[k][tid];
+#pragma unroll
+    for (int j = 0; j < IGP_T; ++j) {
+      const int igp = igpt * IGP_T + j;
+      const bool v = vig && igp < p.ngpown;
+      const size_t off = static_cast<size_t>(min(igp, p.ngpown - 1)) * p.ncouls + igc;
+      const double2 wt = __ldg(p.wtilde + off);
+      const double2 e = v ? __ldg(p.eps + off) : make_double2(0.0, 0.0);
+      const double wt2 = fma(wt.x, wt.x, wt.y * wt.y);
+      const double c1r = e.x * wt.x - e.y * wt.y, c1i = e.x * wt.y + e.y * wt.x;  // eps wt
+      const double c2r = e.x * wt2, c2i = e.y * wt2;                              // eps |wt|^2
+      const double rw = item_regular ? (wt2 > 0.0 ? 1.0 / sqrt(wt2) : 0.0) : 1.0;
+      const double cfr = e.x * rw, cfi = e.y * rw;                                // eps / |wt|
+#pragma unroll
+      for (int iw = 0; iw < NW; ++iw) {
+        const double2 u = S1[j][iw], w = S2[j][iw], f = Sf[j][iw];
+        a[4 * iw + 0] += (c1r * u.x - c1i * u.y) - (c2r * w.x - c2i * w.y);
+        a[4 * iw + 1] += (c1r * u.y + c1i * u.x) - (c2r * w.y + c2i * w.x);
+        a[4 * iw + 2] += cfr * f.x - cfi * f.y;
+        a[4 * iw + 3] += cfr * f.y + cfi * f.x;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4 * NW; ++k) s_acc[k][tid] = a[k];
+  }
+
+  Acc<NW> acc;
+#pragma unroll
+  for (int iw = 0; iw < NW; ++iw) {
+    acc.a[iw] = make_double2(s_acc[4 * iw + 0][tid], s_acc[4 * iw + 1][tid]);
+    acc.b[iw] = make_double2(s_acc[4 * iw + 2][tid], s_acc[4 * iw + 3][tid]);
+  }
+  acc.nn = cnt.nn;
+  acc.nf = cnt.nf;
+  block_reduce_write<NW, COUNT>(acc, p.partials, p.cpartials, 1ull);
+}
+
 // Sum the per-CTA partials in a fixed order and form achtemp/asxtemp for the
 // frequency group [iw0, iw0 + NW).  out: [ach(2 nw_total) | asx(2 nw_total)],
 // counts: [near, far] (accumulated over frequency groups: `first` zeroes).

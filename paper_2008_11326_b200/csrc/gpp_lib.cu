@@ -209,6 +209,22 @@ KernelFn pick_plain(int nw) {
   }
 }
 
+// Production kernel: igp tile per frequency-group size, the largest tile
+// whose S sums fit the 128-register budget without spills (ptxas -v).
+// Four-frequency groups keep the one-seed kernel (FastPolicy3): their S sums
+// do not fit beside the ach/asx shared-memory slab.
+int sacc_igp(int nw) { return nw <= 1 ? 4 : (nw == 2 ? 3 : (nw == 3 ? 2 : 3)); }
+
+template <bool C>
+KernelFn pick_sacc(int nw) {
+  switch (nw) {
+    case 1: return gpp::gpp_sacc_kernel<1, 4, C>;
+    case 2: return gpp::gpp_sacc_kernel<2, 3, C>;
+    case 3: return gpp::gpp_sacc_kernel<3, 2, C>;
+    default: return gpp::gpp_main_kernel<gpp::FastPolicy, 4, 3, C>;
+  }
+}
+
 template <bool C>
 KernelFn pick_kernel_c(int variant, int nw, int igp_t) {
   switch (variant) {
@@ -216,7 +232,8 @@ KernelFn pick_kernel_c(int variant, int nw, int igp_t) {
     case GPP_VARIANT_RCP: return pick_plain<gpp::PlainPolicy<1>, C>(nw);
     case GPP_KERNEL_SQ_SPLIT: return pick_fast_nw<gpp::FastPolicyT<0, 2>, C>(nw, igp_t);
     case GPP_KERNEL_IW_HOIST: return pick_fast_nw<gpp::FastPolicyT<1, 3>, C>(nw, igp_t);
-    default: return pick_fast_nw<gpp::FastPolicy, C>(nw, igp_t);
+    case GPP_KERNEL_ONE_SEED: return pick_fast_nw<gpp::FastPolicy, C>(nw, igp_t);
+    default: return pick_sacc<C>(nw);
   }
 }
 
@@ -256,6 +273,8 @@ int make_plan_uncached(gpp_ctx* c, int variant, int nw_group, bool count, Plan* 
   const Tune tune = read_tune();
   if (variant == GPP_VARIANT_DIV || variant == GPP_VARIANT_RCP)
     pl->igp_t = 2;  // the only instantiation of the plain kernels
+  else if (variant == GPP_VARIANT_RCP_SQ)
+    pl->igp_t = sacc_igp(nw_group);
   else
     pl->igp_t = fast_igp(nw_group, tune.igp >= 2 && tune.igp <= 4 ? tune.igp
                                                                   : choose_igp_tile(c->ngpown));
@@ -393,9 +412,9 @@ int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool
 }
 
 int check_variant(int32_t variant) {
-  if (variant < GPP_VARIANT_DIV || variant > GPP_KERNEL_IW_HOIST)
+  if (variant < GPP_VARIANT_DIV || variant > GPP_KERNEL_ONE_SEED)
     return fail(GPP_ERR_ARG, "unknown variant " + std::to_string(variant) +
-                                 " (expected 0=div, 1=rcp, 2=rcp_sq, 3/4 = ladder kernels)");
+                                 " (expected 0=div, 1=rcp, 2=rcp_sq, 3..5 = ladder kernels)");
   return GPP_OK;
 }
 

@@ -88,8 +88,8 @@ B200_KERNEL = {
     "v4": "rcp_sq/split",   # band innermost (all B200 kernels)
     "v5": "rcp_sq/iw",      # per-tuple eps*t, P, Q reused across iw
     "v6": "rcp_sq/iw",      # cache blocking (smem staging, cp.async ring)
-    "v7": "rcp_sq/iw",      # aqsmtemp tile transposed in shared memory
-    "v8": "rcp_sq",         # single rsqrt seed, regular-item fast path, tuned occupancy
+    "v7": "rcp_sq/seed",    # single rsqrt seed for 1/d and sqrt(d), far == !near
+    "v8": "rcp_sq",         # per-(igp, iw) band sums, constants once per item
 }
 
 
