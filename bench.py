@@ -424,7 +424,7 @@ def run_ours(args, dist: Dist):
             "frac": achieved / peak_tf,
             "traffic": prof.get("dram_bytes_per_launch"),
             "peak_source": "measured live: DFMA microbenchmark (gpp_fp64_peak) on this GPU in this run",
-            "kernel": "gpp_main_kernel<FastPolicy>",
+            "kernel": "gpp_sacc_kernel (rcp_sq production kernel)",
             "kernel_ms": t_main_ms,
             "algorithmic_flops_per_launch": flops_job / dist.world,
             "fma_ratio_analytic": None,

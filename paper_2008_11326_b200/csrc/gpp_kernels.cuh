@@ -34,7 +34,7 @@
 namespace gpp {
 
 constexpr int kThreads = 256;     // threads per CTA (= ig per item)
-constexpr int kMaxChunk = 64;     // bands per item (upper bound)
+constexpr int kMaxChunk = 128;    // bands per item (upper bound)
 constexpr int kMaxIgpTile = 4;    // igp per thread (upper bound)
 constexpr int kMaxNwGroup = 4;    // frequencies per launch (host loops groups)
 constexpr int kAnDepth = 4;       // aqsntemp bands in flight per thread (cp.async ring)
