@@ -153,6 +153,13 @@ int gpp_evaluate_host(gpp_ctx* ctx, int32_t variant, int64_t nbands, int64_t ngp
 int gpp_run_factored(gpp_ctx* ctx, int32_t variant, double* achtemp, double* asxtemp,
                      int64_t* near_far, float* ms);
 
+/* variant_terms (rooflab/gpp/kernel.py:63-95) of the uploaded problem: the
+ * per-(iw, ig, igp) branch terms sch, ssx (complex, interleaved) and the
+ * near / far decision masks (0/1 bytes), C-order (nw, ncouls, ngpown) as the
+ * reference returns them.  Band-invariant wx only (GPP_ERR_ARG otherwise). */
+int gpp_variant_terms(gpp_ctx* ctx, int32_t variant, double* sch, double* ssx, uint8_t* near_mask,
+                      uint8_t* far_mask);
+
 /* Device-resident timing: `iters` back-to-back evaluations on the context's
  * stream (compute kernels + finalize + allreduce when attached, no host
  * copies).  total_ms = event time of the whole run; main_ms = summed event

@@ -58,6 +58,11 @@ SIGNATURES = {
         ctypes.c_int,
         [ctypes.c_void_p, ctypes.c_int32, _c_double_p, _c_double_p, _c_i64_p, _c_float_p],
     ),
+    "gpp_variant_terms": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.c_int32, _c_double_p, _c_double_p, ctypes.POINTER(ctypes.c_uint8),
+         ctypes.POINTER(ctypes.c_uint8)],
+    ),
     "gpp_time": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, _c_float_p, _c_float_p]),
     "gpp_kernel_info": (
         ctypes.c_int,

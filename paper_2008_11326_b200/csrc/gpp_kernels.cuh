@@ -986,6 +986,38 @@ __global__ void __launch_bounds__(256) gpp_synth_kernel(U128 state0, U128 inc,
   }
 }
 
+// variant_terms (rooflab/gpp/kernel.py:63-95) on the device: per (iw, ig,
+// igp) the branch terms sch, ssx and the decision masks of variant V, laid
+// out (nw, ncouls, ngpown) in C order as the reference returns them.
+// wtilde/eps are F-order (ig fastest), so element (ig, igp) = e % nc, e / nc.
+template <int V>
+__global__ void __launch_bounds__(kThreads) gpp_variant_terms_kernel(
+    const double2* __restrict__ wtilde, const double2* __restrict__ eps,
+    const double* __restrict__ wx0, int nw, long long ncouls, long long ngpown, double2* sch,
+    double2* ssx, unsigned char* near_out, unsigned char* far_out) {
+  const long long n_el = ncouls * ngpown;
+  for (long long e = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x; e < n_el;
+       e += static_cast<long long>(gridDim.x) * kThreads) {
+    const long long ig = e % ncouls, igp = e / ncouls;
+    const typename PlainPolicy<V>::St st = PlainPolicy<V>::make(__ldg(wtilde + e), __ldg(eps + e), true);
+    for (int iw = 0; iw < nw; ++iw) {
+      // One instance with t = 1: acc.a = sch, acc.b = ssx.
+      Acc<1> acc;
+      acc.a[0] = make_double2(0.0, 0.0);
+      acc.b[0] = make_double2(0.0, 0.0);
+      acc.nn = 0;
+      acc.nf = 0;
+      const double wx[1] = {__ldg(wx0 + iw)};
+      PlainPolicy<V>::template tuple<1, true, false>(st, 1.0, 0.0, wx, acc);
+      const long long o = (static_cast<long long>(iw) * ncouls + ig) * ngpown + igp;
+      sch[o] = acc.a[0];
+      ssx[o] = acc.b[0];
+      near_out[o] = static_cast<unsigned char>(acc.nn);
+      far_out[o] = static_cast<unsigned char>(acc.nf);
+    }
+  }
+}
+
 // FP64 pipe peak: 8 independent DFMA chains per thread, a = a * a + c.
 // One register operand per DFMA keeps the operand collector out of the way
 // (a DFMA with three distinct register operands runs at 2/3 rate on B200,

@@ -927,6 +927,53 @@ int gpp_run_factored(gpp_ctx* c, int32_t variant, double* achtemp, double* asxte
   return GPP_OK;
 }
 
+int gpp_variant_terms(gpp_ctx* c, int32_t variant, double* sch, double* ssx, uint8_t* near_mask,
+                      uint8_t* far_mask) {
+  if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
+  if (variant < GPP_VARIANT_DIV || variant > GPP_VARIANT_RCP_SQ)
+    return fail(GPP_ERR_ARG, "variant_terms takes a reference variant (0=div, 1=rcp, 2=rcp_sq)");
+  if (!sch || !ssx || !near_mask || !far_mask) return fail(GPP_ERR_ARG, "output pointer is NULL");
+  if (!c->have_problem) return fail(GPP_ERR_ARG, "no problem uploaded");
+  if (!c->wx_band_invariant)
+    return fail(GPP_ERR_ARG, "variant_terms needs a band-invariant wx (the reference's (nw,) vector)");
+  DeviceGuard g(c->device);
+  if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
+  const size_t n = static_cast<size_t>(c->nw) * c->ncouls * c->ngpown;
+  DevBuf<double2> d_sch, d_ssx;
+  DevBuf<unsigned char> d_near, d_far;
+  int rc = GPP_OK;
+  do {
+    cudaError_t e = d_sch.ensure(n);
+    if (e == cudaSuccess) e = d_ssx.ensure(n);
+    if (e == cudaSuccess) e = d_near.ensure(n);
+    if (e == cudaSuccess) e = d_far.ensure(n);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "variant_terms buffers"); break; }
+    const long long n_el = c->ncouls * c->ngpown;
+    const int grid = static_cast<int>(std::max<long long>(
+        1, std::min<long long>(c->num_sms * 8, (n_el + gpp::kThreads - 1) / gpp::kThreads)));
+#define GPP_VT(V)                                                                              \
+  gpp::gpp_variant_terms_kernel<V><<<grid, gpp::kThreads, 0, c->stream>>>(                     \
+      c->wtilde.ptr, c->eps.ptr, c->wxb.ptr, c->nw, c->ncouls, c->ngpown, d_sch.ptr, d_ssx.ptr, \
+      d_near.ptr, d_far.ptr)
+    if (variant == GPP_VARIANT_DIV) GPP_VT(0);
+    else if (variant == GPP_VARIANT_RCP) GPP_VT(1);
+    else GPP_VT(2);
+#undef GPP_VT
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(sch, d_sch.ptr, n * sizeof(double2), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ssx, d_ssx.ptr, n * sizeof(double2), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(near_mask, d_near.ptr, n, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(far_mask, d_far.ptr, n, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) rc = cuda_fail(e, "variant_terms");
+  } while (0);
+  d_sch.release();
+  d_ssx.release();
+  d_near.release();
+  d_far.release();
+  return rc;
+}
+
 int gpp_comm_init_all(gpp_ctx** ctxs, int n) {
   if (!ctxs || n < 1) return fail(GPP_ERR_ARG, "need at least one context");
   std::vector<int> devs(n);

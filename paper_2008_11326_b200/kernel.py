@@ -315,6 +315,45 @@ def reference_result(problem, device: int = 0) -> GPPResult:
     return evaluate(problem, "div", device, counts=False)[0]
 
 
+class VariantTerms:
+    """Per-(iw, ig, igp) branch terms (rooflab/gpp/kernel.py:48-60)."""
+
+    def __init__(self, sch, ssx, near, far):
+        self.sch, self.ssx, self.near, self.far = sch, ssx, near, far
+
+
+def variant_terms(problem, variant: str, device: int = 0) -> VariantTerms:
+    """Drop-in for rooflab.gpp.kernel.variant_terms (kernel.py:63-95),
+    computed on the GPU; arrays of shape (nw, ncouls, ngpown)."""
+    _reference_variant(variant)
+    ctx = get_context(device)
+    ctx.upload(problem)
+    nw, nc, ng = ctx.nw, int(problem.ncouls), int(problem.ngpown)
+    sch = np.empty((nw, nc, ng), dtype=np.complex128)
+    ssx = np.empty((nw, nc, ng), dtype=np.complex128)
+    near = np.empty((nw, nc, ng), dtype=np.uint8)
+    far = np.empty((nw, nc, ng), dtype=np.uint8)
+    u8 = ctypes.POINTER(ctypes.c_uint8)
+    _lib.check(ctx._lib.gpp_variant_terms(ctx._h, _variant_code(variant),
+                                          sch.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                          ssx.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                          near.ctypes.data_as(u8), far.ctypes.data_as(u8)),
+               "gpp_variant_terms")
+    return VariantTerms(sch, ssx, near.astype(bool), far.astype(bool))
+
+
+def complex_reciprocal(z):
+    """1/z as conj(z) / |z|^2 (rooflab/gpp/kernel.py:33-45); host-side helper."""
+    from .problem import TOL_ZERO
+
+    arr = np.asarray(z)
+    denom = arr.real * arr.real + arr.imag * arr.imag
+    if np.any(denom <= TOL_ZERO * TOL_ZERO):
+        raise DomainError("complex_reciprocal: input magnitude at or below tol_zero")
+    out = np.conj(arr) * (1.0 / denom)
+    return out if isinstance(z, np.ndarray) else complex(out)
+
+
 def evaluate_factored(problem, variant: str = "rcp_sq", device: int = 0) -> GPPResult:
     """The reference's production algorithm (kernel.py:98-114: ZGEMM of the
     band weights, then the branch terms) on the GPU.  Time-to-solution path

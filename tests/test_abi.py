@@ -170,3 +170,16 @@ def test_golden_roundtrip_and_max_rel_error(tmp_path):
     zero = type(g)(achtemp=np.zeros(2, complex), asxtemp=np.zeros(2, complex))
     with pytest.raises(DomainError):
         max_rel_error(g, zero)
+
+
+def test_complex_reciprocal_mirror():
+    """kernel.py:33-45 mirror: test_gpp.py:164-184 restated."""
+    from paper_2008_11326_b200 import complex_reciprocal
+
+    rng = np.random.default_rng(5)
+    z = rng.uniform(0.1, 10.0, 100_000) * np.exp(1j * rng.uniform(0.0, 2 * np.pi, 100_000))
+    rel = np.abs(complex_reciprocal(z) - 1.0 / z) / np.abs(1.0 / z)
+    assert float(rel.max()) <= 4 * np.finfo(np.float64).eps
+    with pytest.raises(DomainError):
+        complex_reciprocal(0j)
+    assert complex_reciprocal(2 + 0j) == 0.5 + 0j

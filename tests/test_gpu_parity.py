@@ -341,3 +341,18 @@ def test_device_synthesis_is_bitexact(dims, seed, nw, br):
     finally:
         a.close()
         b.close()
+
+
+@pytest.mark.parametrize("variant", ["div", "rcp", "rcp_sq"])
+def test_variant_terms_vs_oracle(variant):
+    """GPU variant_terms (kernel.py:63-95): masks exact, terms to rounding."""
+    from paper_2008_11326_b200 import variant_terms
+
+    for dims, seed, nw in (((4, 7, 300), 1, 2), ((3, 13, 129), 7, 3)):
+        p = synth_problem(*dims, seed=seed, nw=nw)
+        got = variant_terms(p, variant)
+        sch, ssx, near, far = orc.variant_terms(p, variant)
+        assert np.array_equal(got.near, near) and np.array_equal(got.far, far)
+        scale = max(np.abs(sch).max(), np.abs(ssx).max())
+        assert np.abs(got.sch - sch).max() <= 1e-14 * scale
+        assert np.abs(got.ssx - ssx).max() <= 1e-14 * scale
