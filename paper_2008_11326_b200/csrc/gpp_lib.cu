@@ -289,13 +289,28 @@ int make_plan_uncached(gpp_ctx* c, int variant, int nw_group, bool count, Plan* 
   pl->blocks_per_sm = std::max(bps, 1);
   if (tune.bps > 0) pl->blocks_per_sm = std::min(pl->blocks_per_sm, tune.bps);
   const long long slots = static_cast<long long>(pl->blocks_per_sm) * c->num_sms;
-  // Band chunk: as long as possible (amortises the per-item state load) while
-  // leaving >= 32 items per resident CTA so the static round-robin balances.
-  int bchunk = static_cast<int>(std::min<int64_t>(gpp::kMaxChunk, c->nbands));
+  // Band chunk: minimise the modelled makespan of the static round-robin,
+  //   ceil(items / resident CTAs) * (chunk + kItemOverheadBands),
+  // where an item's fixed cost (state load, staging, barrier, epilogue) was
+  // measured at ~4 bands' worth of work (tools/probe_shard.py: step time of
+  // 1/N band shards).  Long chunks amortise that cost; short ones balance
+  // small shards across the 148 SMs.
+  constexpr double kItemOverheadBands = 4.0;
   auto items_for = [&](int bc) {
     return static_cast<long long>(pl->n_igblk) * pl->n_igptile * ((c->nbands + bc - 1) / bc);
   };
-  while (bchunk > 8 && items_for(bchunk) < 32 * slots) bchunk = (bchunk + 1) / 2;
+  int bchunk = 8;
+  double best = -1.0;
+  for (int bc = 8; bc <= gpp::kMaxChunk; bc *= 2) {
+    const int eff = static_cast<int>(std::min<int64_t>(bc, c->nbands));
+    const long long waves = (items_for(eff) + slots - 1) / slots;
+    const double cost = static_cast<double>(waves) * (eff + kItemOverheadBands);
+    if (best < 0.0 || cost < best) {
+      best = cost;
+      bchunk = eff;
+    }
+    if (eff >= c->nbands) break;
+  }
   pl->bchunk = bchunk;
   pl->n_items = items_for(bchunk);
   pl->grid = static_cast<int>(std::min<long long>(slots, pl->n_items));
