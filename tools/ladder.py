@@ -6,7 +6,7 @@ report device time and the version's algorithmic FLOP rate (the reference's
 own per-version counters, kernel.py:191-212).  With --ncu, every version is
 launched exactly once after one counting launch, for
 
-    ncu --metrics <list> -k regex:gpp_main_kernel -s 1 -c 9 python tools/ladder.py --ncu
+    ncu --metrics <list> -k regex:"gpp_main_kernel|gpp_sacc_kernel" -s 1 -c 9 python tools/ladder.py --ncu
 
 whose CSV tools/ncu_to_rooflab.py turns into the reference's metrics format.
 """

@@ -19,6 +19,6 @@ p = synth_problem(*a.dims, seed=a.seed, nw=a.nw, check=False)
 ctx = GPPContext(0)
 ctx.upload(p)
 # The production (uncounted) kernel, as evaluate_variant and bench.py run it:
-# profile with -k regex:gpp_main_kernel -s 1 -c 1 to capture the second launch.
+# profile with -k regex:gpp_sacc_kernel -s 1 -c 1 to capture the second launch.
 tot, main = ctx.time(a.variant, a.reps)
 print(a.variant, a.dims, "nw", a.nw, f"{main / a.reps:.3f} ms per launch")
