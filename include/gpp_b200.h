@@ -129,9 +129,10 @@ int gpp_synth(gpp_ctx* ctx, int64_t nbands, int64_t ngpown, int64_t ncouls, int3
 
 /* Upload + evaluate in one call, with the host->device copy pipelined
  * against the computation: the ig rows of wtilde / i_eps / aqsntemp are
- * copied in `slabs` ig slabs (<= 0: 16) on a copy stream, and the kernel for
- * slab s starts as soon as its rows have landed, while slab s+1 is in
- * flight.  Arguments as gpp_upload + gpp_run; `ms` (nullable) receives the
+ * copied in ig slabs on a copy stream, and the kernel for slab s starts as
+ * soon as its rows have landed, while slab s+1 is in flight.  `slabs` > 0:
+ * that many equal slabs; <= 0: slabs tapering towards single 256-ig blocks
+ * at the end, so that little computation follows the last copy.  Arguments as gpp_upload + gpp_run; `ms` (nullable) receives the
  * device time from the first copy to the end of the computation.  Host
  * arrays should be page-locked (gpp_host_register) for the copies to be
  * asynchronous.  Afterwards the problem is resident, as after gpp_upload.

@@ -88,6 +88,8 @@ struct gpp_ctx {
   bool initialized = false;
   cudaStream_t stream = nullptr;
   cudaStream_t cstream = nullptr;  // H2D copies of the pipelined evaluate
+  cudaStream_t kstream2 = nullptr;  // odd ig slabs: overlaps a slab's tail with the next
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> slab_ev;
   int num_sms = 0;
@@ -137,7 +139,10 @@ int ensure_init(gpp_ctx* c) {
   if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
   GPP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   GPP_CUDA(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+  GPP_CUDA(cudaStreamCreateWithFlags(&c->kstream2, cudaStreamNonBlocking));
   for (auto& ev : c->ev) GPP_CUDA(cudaEventCreate(&ev));
+  GPP_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  GPP_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   GPP_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
   c->initialized = true;
   return GPP_OK;
@@ -266,6 +271,30 @@ int choose_igp_tile(int64_t ngpown) {
   return cost4 < cost3 ? 4 : 3;
 }
 
+// Band chunk: minimise the modelled makespan of the static round-robin,
+//   ceil(items / resident CTAs) * (chunk + kItemOverheadBands),
+// where an item's fixed cost (state load, staging, barrier, epilogue) was
+// measured at ~4 bands' worth of work (tools/probe_shard.py: step time of
+// 1/N band shards).  Long chunks amortise that cost; short ones balance
+// small shards (and small ig slabs) across the 148 SMs.
+int choose_bchunk(long long n_igblk, long long n_igptile, int64_t nbands, long long slots) {
+  constexpr double kItemOverheadBands = 4.0;
+  int bchunk = 8;
+  double best = -1.0;
+  for (int bc = 8; bc <= gpp::kMaxChunk; bc *= 2) {
+    const int eff = static_cast<int>(std::min<int64_t>(bc, nbands));
+    const long long items = n_igblk * n_igptile * ((nbands + eff - 1) / eff);
+    const long long waves = (items + slots - 1) / slots;
+    const double cost = static_cast<double>(waves) * (eff + kItemOverheadBands);
+    if (best < 0.0 || cost < best) {
+      best = cost;
+      bchunk = eff;
+    }
+    if (eff >= nbands) break;
+  }
+  return bchunk;
+}
+
 int make_plan_uncached(gpp_ctx* c, int variant, int nw_group, bool count, Plan* pl) {
   // The plain (as-written) variants keep two igp per thread and the fast
   // kernel drops to 3 at four frequencies: both choices avoid spills under
@@ -289,30 +318,10 @@ int make_plan_uncached(gpp_ctx* c, int variant, int nw_group, bool count, Plan* 
   pl->blocks_per_sm = std::max(bps, 1);
   if (tune.bps > 0) pl->blocks_per_sm = std::min(pl->blocks_per_sm, tune.bps);
   const long long slots = static_cast<long long>(pl->blocks_per_sm) * c->num_sms;
-  // Band chunk: minimise the modelled makespan of the static round-robin,
-  //   ceil(items / resident CTAs) * (chunk + kItemOverheadBands),
-  // where an item's fixed cost (state load, staging, barrier, epilogue) was
-  // measured at ~4 bands' worth of work (tools/probe_shard.py: step time of
-  // 1/N band shards).  Long chunks amortise that cost; short ones balance
-  // small shards across the 148 SMs.
-  constexpr double kItemOverheadBands = 4.0;
-  auto items_for = [&](int bc) {
-    return static_cast<long long>(pl->n_igblk) * pl->n_igptile * ((c->nbands + bc - 1) / bc);
-  };
-  int bchunk = 8;
-  double best = -1.0;
-  for (int bc = 8; bc <= gpp::kMaxChunk; bc *= 2) {
-    const int eff = static_cast<int>(std::min<int64_t>(bc, c->nbands));
-    const long long waves = (items_for(eff) + slots - 1) / slots;
-    const double cost = static_cast<double>(waves) * (eff + kItemOverheadBands);
-    if (best < 0.0 || cost < best) {
-      best = cost;
-      bchunk = eff;
-    }
-    if (eff >= c->nbands) break;
-  }
+  const int bchunk = choose_bchunk(pl->n_igblk, pl->n_igptile, c->nbands, slots);
   pl->bchunk = bchunk;
-  pl->n_items = items_for(bchunk);
+  pl->n_items = static_cast<long long>(pl->n_igblk) * pl->n_igptile *
+                ((c->nbands + bchunk - 1) / bchunk);
   pl->grid = static_cast<int>(std::min<long long>(slots, pl->n_items));
   return GPP_OK;
 }
@@ -379,10 +388,19 @@ int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool
     KernelFn fn = pick_kernel(variant, nwg, pl.igp_t, count);
     int rows = 0;  // partial rows written by this frequency group
     if (ev_main && gi == 0) GPP_CUDA(cudaEventRecord(ev_main[0], c->stream));
+    // Slabs alternate between two streams so that slab s+1's CTAs fill the
+    // SMs that slab s's last wave leaves idle (each slab writes its own
+    // partial rows; the finalize joins both streams).
+    const bool two = n_slabs > 1;
+    if (two) {
+      GPP_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+      GPP_CUDA(cudaStreamWaitEvent(c->kstream2, c->ev_fork, 0));
+    }
     for (int s = 0; s < n_slabs; ++s) {
       const int nblk = sl.blk0[s + 1] - sl.blk0[s];
       if (nblk <= 0) continue;
-      if (gi == 0 && !sl.ready.empty()) GPP_CUDA(cudaStreamWaitEvent(c->stream, sl.ready[s], 0));
+      cudaStream_t ks = (two && (s & 1)) ? c->kstream2 : c->stream;
+      if (gi == 0 && !sl.ready.empty()) GPP_CUDA(cudaStreamWaitEvent(ks, sl.ready[s], 0));
       gpp::Params p;
       p.wtilde = c->wtilde.ptr;
       p.eps = c->eps.ptr;
@@ -397,15 +415,25 @@ int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool
       p.igblk0 = sl.blk0[s];
       p.n_igblk = nblk;
       p.n_igptile = pl.n_igptile;
-      p.bchunk = pl.bchunk;
-      p.n_items = pl.n_items / pl.n_igblk * nblk;
+      // A slab re-plans its band chunk for its own item count: short chunks
+      // keep the last (small) slabs from idling most of the SMs.
+      p.bchunk = nblk == pl.n_igblk
+                     ? pl.bchunk
+                     : choose_bchunk(nblk, pl.n_igptile, c->nbands,
+                                     static_cast<long long>(pl.blocks_per_sm) * c->num_sms);
+      p.n_items = static_cast<long long>(nblk) * pl.n_igptile *
+                  ((c->nbands + p.bchunk - 1) / p.bchunk);
       p.wxmax = c->wxmax;
       const int grid = static_cast<int>(std::min<long long>(pl.grid, p.n_items));
       p.partials = c->partials.ptr + static_cast<size_t>(rows) * 4 * nwg;
       p.cpartials = c->cpartials.ptr + static_cast<size_t>(rows) * 2;
-      fn<<<grid, gpp::kThreads, 0, c->stream>>>(p);
+      fn<<<grid, gpp::kThreads, 0, ks>>>(p);
       GPP_CUDA(cudaGetLastError());
       rows += grid;
+    }
+    if (two) {
+      GPP_CUDA(cudaEventRecord(c->ev_join, c->kstream2));
+      GPP_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     }
     if (ev_main && gi + 1 == groups.size()) GPP_CUDA(cudaEventRecord(ev_main[1], c->stream));
     pick_finalize(nwg)<<<1, 256, 0, c->stream>>>(c->partials.ptr, c->cpartials.ptr, rows,
@@ -465,6 +493,7 @@ void gpp_destroy(gpp_ctx* c) {
     DeviceGuard g(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->cstream) cudaStreamSynchronize(c->cstream);
+    if (c->kstream2) cudaStreamSynchronize(c->kstream2);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->blas) cublasDestroy(c->blas);
     c->weight.release();
@@ -483,6 +512,9 @@ void gpp_destroy(gpp_ctx* c) {
     for (auto& ev : c->ev)
       if (ev) cudaEventDestroy(ev);
     for (auto& ev : c->slab_ev) cudaEventDestroy(ev);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->kstream2) cudaStreamDestroy(c->kstream2);
     if (c->cstream) cudaStreamDestroy(c->cstream);
     if (c->stream) cudaStreamDestroy(c->stream);
   }
@@ -605,6 +637,58 @@ int copy_rows(gpp_ctx* c, const HostProblem& h, int64_t i0, int64_t i1, cudaStre
   return GPP_OK;
 }
 
+// ig-slab schedule of the pipelined evaluate, as block offsets.  slabs > 0:
+// that many equal slabs.  slabs <= 0: a taper -- slab sizes shrink by 1/1.2
+// towards the end, down to single 256-ig blocks.  The copy is the critical
+// path (PCIe ~55 GB/s vs the kernel's ~0.8 of that time); what follows the
+// last byte is the kernel on the last slab, so it should be small, while
+// every earlier slab's kernel must fit inside the next slab's copy (ratio
+// >= 0.8) and the slab count stays low (each 2D copy row costs ~20 ns).
+// tools/probe_slabs.py: 6.43 ms end to end at paper size vs 6.74 ms for 16
+// equal slabs.  GPP_SLABS="b0,b1,..." (block counts summing to the block
+// total) overrides, for experiments.
+std::vector<int> slab_schedule(int n_blk, int slabs) {
+  std::vector<int> sizes;
+  if (const char* e = std::getenv("GPP_SLABS")) {
+    int sum = 0;
+    for (const char* q = e; *q;) {
+      char* end = nullptr;
+      const long v = std::strtol(q, &end, 10);
+      if (end == q || v <= 0) break;
+      sizes.push_back(static_cast<int>(v));
+      sum += static_cast<int>(v);
+      q = *end == ',' ? end + 1 : end;
+    }
+    if (sum != n_blk) sizes.clear();
+  }
+  if (sizes.empty() && slabs > 0) {
+    const int n = std::min(slabs, n_blk);
+    for (int i = 0; i < n; ++i)
+      sizes.push_back(static_cast<int>(static_cast<int64_t>(n_blk) * (i + 1) / n -
+                                       static_cast<int64_t>(n_blk) * i / n));
+  }
+  if (sizes.empty()) {
+    // Built from the end: 1, 1, 2, 3, 4, 5, 6, 8, 10, 12, 15, 18, 22, ...
+    std::vector<int> rev{1};
+    int sum = 1, sz = 1;
+    if (n_blk > 1) {
+      rev.push_back(1);
+      sum = 2;
+    }
+    while (sum < n_blk) {
+      sz = std::max(sz + 1, static_cast<int>(std::ceil(sz * 1.2)));
+      rev.push_back(sz);
+      sum += sz;
+    }
+    rev.back() -= sum - n_blk;  // the first slab takes the remainder
+    if (rev.back() <= 0) rev.pop_back();
+    sizes.assign(rev.rbegin(), rev.rend());
+  }
+  std::vector<int> blk0{0};
+  for (int v : sizes) blk0.push_back(blk0.back() + v);
+  return blk0;
+}
+
 int finish_run(gpp_ctx* c, double* achtemp, double* asxtemp, int64_t* near_far) {
   if (c->comm && c->nranks > 1) {
     GPP_NCCL(ncclGroupStart());
@@ -678,22 +762,21 @@ int gpp_evaluate_host(gpp_ctx* c, int32_t variant, int64_t nbands, int64_t ngpow
   if (rc) return rc;
   // ig slabs on 256-ig block boundaries.
   const int n_blk = static_cast<int>((ncouls + gpp::kThreads - 1) / gpp::kThreads);
-  const int n_sl = std::max(1, std::min<int>(slabs > 0 ? slabs : 16, n_blk));
-  while (static_cast<int>(c->slab_ev.size()) < n_sl + 1) {
+  SlabSched sched;
+  sched.blk0 = slab_schedule(n_blk, slabs);
+  const int n_sched = static_cast<int>(sched.blk0.size()) - 1;
+  while (static_cast<int>(c->slab_ev.size()) < n_sched + 1) {
     cudaEvent_t e;
     GPP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c->slab_ev.push_back(e);
   }
-  SlabSched sched;
-  for (int sl = 0; sl <= n_sl; ++sl) sched.blk0.push_back(static_cast<int>(
-      static_cast<int64_t>(n_blk) * sl / n_sl));
   // Copy stream: small arrays, then the ig rows slab by slab, each slab
-  // signalling the compute stream; the compute stream runs slab s while the
-  // rows of slab s+1 are in flight.
+  // signalling the compute streams (two, alternating); slab s computes while
+  // the rows of slab s+1 are in flight.
   GPP_CUDA(cudaEventRecord(c->ev[2], c->cstream));
   rc = copy_small(c, h, c->cstream);
   if (rc) return rc;
-  for (int sl = 0; sl < n_sl; ++sl) {
+  for (int sl = 0; sl < n_sched; ++sl) {
     const int64_t i0 = static_cast<int64_t>(sched.blk0[sl]) * gpp::kThreads;
     const int64_t i1 = std::min<int64_t>(ncouls, static_cast<int64_t>(sched.blk0[sl + 1]) * gpp::kThreads);
     rc = copy_rows(c, h, i0, i1, c->cstream);

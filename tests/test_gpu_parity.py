@@ -216,7 +216,7 @@ def test_irregular_items_take_the_general_path():
         assert max_rel_error(r, want) <= TOL
 
 
-@pytest.mark.parametrize("slabs", [1, 3, 8, 1000])
+@pytest.mark.parametrize("slabs", [0, 1, 3, 8, 1000])
 def test_pipelined_host_evaluate(slabs):
     """gpp_evaluate_host: H2D by ig slabs overlapped with the kernel; same
     result as upload + run (bitwise: same items, same partial order per slab
@@ -234,6 +234,28 @@ def test_pipelined_host_evaluate(slabs):
         part, _, _ = ctx.evaluate_host(p, "rcp_sq", band_range=(10, 30), slabs=slabs)
         ref = orc.reference_result(__import__("paper_2008_11326_b200.dist", fromlist=["x"]).shard_problem(p, 10, 30))
         assert max_rel_error(part, ref) <= TOL
+    finally:
+        ctx.close()
+
+
+@pytest.mark.parametrize("nw", [3, 6])
+def test_pipelined_taper_two_streams(nw):
+    """The default (tapered) slab schedule over 40 ig blocks: slabs alternate
+    between two compute streams, and with nw = 6 the second frequency group's
+    slabs must wait for the first group's finalize.  Oracle parity, exact
+    counts, and bitwise repeatability of the pipelined path."""
+    p = synth_problem(24, 5, 40 * 256 - 17, seed=3, nw=nw)
+    want = orc.reference_result(p)
+    inst, near, far = orc.branch_stats(p, "rcp_sq")
+    ctx = GPPContext(0)
+    try:
+        got, nf, _ = ctx.evaluate_host(p, "rcp_sq", counts=True)
+        assert max_rel_error(got, want) <= TOL
+        assert nf == (near, far)
+        for _ in range(3):
+            again, _, _ = ctx.evaluate_host(p, "rcp_sq", counts=True)
+            assert np.array_equal(again.achtemp, got.achtemp)
+            assert np.array_equal(again.asxtemp, got.asxtemp)
     finally:
         ctx.close()
 
