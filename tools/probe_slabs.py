@@ -31,7 +31,9 @@ for _ in range(10):
 print(f"upload alone {(time.perf_counter() - t0) / 10 * 1e3:7.3f} ms", flush=True)
 n = 128
 cases = [("default", 0, None)] + [("uniform", k, None) for k in (8, 16, 32)]
-for m in (16, 24, 128):
+if os.environ.get("SHORT"):
+    cases = cases[:3]
+for m in (() if os.environ.get("SHORT") else (16, 24, 128)):
     for r in (1.15, 1.2, 1.25):
         cases.append(("taper", 0, taper(n, m, r)))
 for kind, k, sizes in cases:
