@@ -35,6 +35,10 @@ namespace gpp {
 
 constexpr int kThreads = 256;     // threads per CTA (= ig per item)
 constexpr int kMaxChunk = 128;    // bands per item (upper bound)
+#ifndef GPP_SACC_CHUNK
+#define GPP_SACC_CHUNK 256
+#endif
+constexpr int kSaccChunk = GPP_SACC_CHUNK;  // bands per item of gpp_sacc_kernel (upper bound)
 constexpr int kMaxIgpTile = 4;    // igp per thread (upper bound)
 constexpr int kMaxNwGroup = 4;    // frequencies per launch (host loops groups)
 constexpr int kAnDepth = 4;       // aqsntemp bands in flight per thread (cp.async ring)
@@ -48,11 +52,40 @@ struct Params {
   int ncouls, ngpown, nbands;
   int nw_total, iw0;       // this launch evaluates iw in [iw0, iw0 + NW)
   int igblk0;              // first 256-ig block of this launch (ig slab)
+  int band0;               // first (local) band of this launch's band window (gpp_sacc_kernel)
   int n_igblk, n_igptile, bchunk;
   long long n_items;
+  // Division by n_igptile / n_igblk as multiply-shift (host: fastdiv_init), so
+  // that gpp_sacc_kernel decomposes its items on the uniform datapath and the
+  // band offset indexing the WxTable stays in a uniform register.
+  unsigned long long igpt_mul, igblk_mul;
+  int igpt_shift, igblk_shift;
   double wxmax;            // max |wx| over the uploaded bands (regular-item guard)
   double* partials;                 // [gridDim.x][4 * NW]
   unsigned long long* cpartials;    // [gridDim.x][2]
+};
+
+// floor(n / d) for 0 <= n < 2^31 with m = ceil(2^(32+l) / d), l = ceil(log2 d):
+// the error term n (m d - 2^(32+l)) < 2^31 d <= 2^(32+l) stays below one unit.
+__host__ __device__ __forceinline__ unsigned fastdiv(unsigned n, unsigned long long m, int shift) {
+  return static_cast<unsigned>((static_cast<unsigned long long>(n) * m) >> shift);
+}
+inline void fastdiv_init(unsigned d, unsigned long long* m, int* shift) {
+  int l = 0;
+  while ((1ull << l) < d) ++l;
+  *shift = 32 + l;
+  *m = ((1ull << (32 + l)) + d - 1) / d;
+}
+
+// wx of one launch's band window, passed by value as a __grid_constant__
+// kernel parameter: w[(band - band0) * NW + (iw - iw0)].  The band loop's
+// reads of it are warp-uniform with a uniform index, so ptxas serves them
+// with LDCU into uniform registers and the DADD / DMUL that consume wx take
+// it as a UR operand -- one 64-bit register-file read fewer per use in this
+// register-file-read-bound loop, and no shared-memory staging of wx.
+constexpr int kWxParam = 1536;  // 12 KB: 512 bands at NW = 3, 768 at 2, 1536 at 1
+struct WxTable {
+  double w[kWxParam];
 };
 
 // ---------------------------------------------------------------------------
@@ -632,8 +665,8 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_main_kernel(const Params p) {
 template <int NW, int IGP_T, bool COUNT, bool FAST>
 __device__ __forceinline__ void sacc_band_loop(const double2* anp, int ncouls, int nb,
                                                double2 (&s_an)[kAnDepth][kThreads],
-                                               const double2 (&s_am)[kMaxChunk][IGP_T],
-                                               const double (&s_wx)[kMaxChunk][NW],
+                                               const double2 (&s_am)[kSaccChunk][IGP_T],
+                                               const WxTable& wxt, int wx0,
                                                const double (&wtr)[IGP_T],
                                                const double (&wti2)[IGP_T],
                                                const double (&qn)[IGP_T],
@@ -645,15 +678,19 @@ __device__ __forceinline__ void sacc_band_loop(const double2* anp, int ncouls, i
     if (s < nb) cp_async16(&s_an[s][tid], anp + static_cast<size_t>(s) * ncouls);
     cp_async_commit();
   }
+  // Prefetch address advanced incrementally (one 64-bit add per band, not a
+  // wide multiply): four fewer integer instructions in the band loop.
+  const double2* pfp = anp + static_cast<size_t>(kAnDepth - 1) * ncouls;
   for (int bb = 0; bb < nb; ++bb) {
     const int pf = bb + kAnDepth - 1;
-    if (pf < nb) cp_async16(&s_an[pf % kAnDepth][tid], anp + static_cast<size_t>(pf) * ncouls);
+    if (pf < nb) cp_async16(&s_an[pf % kAnDepth][tid], pfp);
+    pfp += ncouls;
     cp_async_commit();
     cp_async_wait<kAnDepth - 1>();
     const double2 an = s_an[bb % kAnDepth][tid];
     double wx[NW];
 #pragma unroll
-    for (int iw = 0; iw < NW; ++iw) wx[iw] = s_wx[bb][iw];
+    for (int iw = 0; iw < NW; ++iw) wx[iw] = wxt.w[wx0 + bb * NW + iw];
 #pragma unroll
     for (int j = 0; j < IGP_T; ++j) {
       const double2 am = s_am[bb][j];
@@ -689,6 +726,18 @@ __device__ __forceinline__ void sacc_band_loop(const double2* anp, int ncouls, i
           // (tools/ab_select.sh: bitwise equal to the exact-select build); it halves
           // the selects (2 SEL instead of 4 FSEL per instance) in this
           // register-file-bound loop: 4.93 -> 4.80 ms at paper size.
+#ifdef GPP_DSETP
+          asm("{\n\t.reg .pred pn;\n\t.reg .b32 il, ih, gl, gh;\n\t"
+              "setp.gt.f64 pn, %2, %3;\n\t"
+              "mov.b64 {il, ih}, %4;\n\t"
+              "mov.b64 {gl, gh}, %5;\n\t"
+              "selp.b32 ih, ih, 0, pn;\n\t"
+              "selp.b32 gh, 0, gh, pn;\n\t"
+              "mov.b64 %0, {il, ih};\n\t"
+              "mov.b64 %1, {gl, gh};\n\t}"
+              : "=d"(in), "=d"(gf)
+              : "d"(d), "d"(qn[j]), "d"(inv), "d"(sq));
+#else
           asm("{\n\t.reg .pred pn;\n\t.reg .b32 il, ih, gl, gh;\n\t"
               "setp.gt.s64 pn, %2, %3;\n\t"
               "mov.b64 {il, ih}, %4;\n\t"
@@ -699,6 +748,7 @@ __device__ __forceinline__ void sacc_band_loop(const double2* anp, int ncouls, i
               "mov.b64 %1, {gl, gh};\n\t}"
               : "=d"(in), "=d"(gf)
               : "l"(__double_as_longlong(d)), "l"(qbits), "d"(inv), "d"(sq));
+#endif
 #ifdef GPP_EXACT_SELECT  // A/B reference build (tools/ab_select.sh): full 64-bit selects
           asm("{\n\t.reg .pred pn;\n\t"
               "setp.gt.s64 pn, %2, %3;\n\t"
@@ -729,9 +779,9 @@ __device__ __forceinline__ void sacc_band_loop(const double2* anp, int ncouls, i
 }
 
 template <int NW, int IGP_T, bool COUNT>
-__global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const Params p) {
-  __shared__ double2 s_am[kMaxChunk][IGP_T];
-  __shared__ double s_wx[kMaxChunk][NW];
+__global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_constant__ Params p,
+                                                               const __grid_constant__ WxTable wxt) {
+  __shared__ double2 s_am[kSaccChunk][IGP_T];
   __shared__ __align__(16) double2 s_an[kAnDepth][kThreads];
   __shared__ double s_acc[4 * NW][kThreads];  // this thread's ach/asx partials
   const int tid = threadIdx.x;
@@ -741,11 +791,13 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const Params p) {
   cnt.nn = 0;
   cnt.nf = 0;
 
-  for (long long item = blockIdx.x; item < p.n_items; item += gridDim.x) {
-    const int igpt = static_cast<int>(item % p.n_igptile);
-    const long long rest = item / p.n_igptile;
-    const int igb = static_cast<int>(rest % p.n_igblk);
-    const int bc = static_cast<int>(rest / p.n_igblk);
+  // n_items < 2^31 (host-checked): items decompose by multiply-shift.
+  for (unsigned item = blockIdx.x; item < static_cast<unsigned>(p.n_items); item += gridDim.x) {
+    const unsigned rest = fastdiv(item, p.igpt_mul, p.igpt_shift);
+    const int igpt = static_cast<int>(item - rest * p.n_igptile);
+    const unsigned bcu = fastdiv(rest, p.igblk_mul, p.igblk_shift);
+    const int igb = static_cast<int>(rest - bcu * p.n_igblk);
+    const int bc = static_cast<int>(bcu);
     const int ig = (p.igblk0 + igb) * kThreads + tid;
     const bool vig = ig < p.ncouls;
     const int igc = vig ? ig : p.ncouls - 1;
@@ -773,12 +825,8 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const Params p) {
       const int bb = k / IGP_T, j = k - bb * IGP_T;
       const int igp = igpt * IGP_T + j;
       s_am[bb][j] = igp < p.ngpown
-                        ? __ldg(p.aqsm + static_cast<size_t>(b0 + bb) * p.ngpown + igp)
+                        ? __ldg(p.aqsm + static_cast<size_t>(p.band0 + b0 + bb) * p.ngpown + igp)
                         : make_double2(0.0, 0.0);
-    }
-    for (int k = tid; k < nb * NW; k += kThreads) {
-      const int bb = k / NW, iw = k - bb * NW;
-      s_wx[bb][iw] = __ldg(p.wxb + static_cast<size_t>(b0 + bb) * p.nw_total + p.iw0 + iw);
     }
     __syncthreads();
 
@@ -791,13 +839,13 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const Params p) {
         S2[j][iw] = make_double2(0.0, 0.0);
         Sf[j][iw] = make_double2(0.0, 0.0);
       }
-    const double2* anp = p.aqsn + static_cast<size_t>(b0) * p.ncouls + igc;
+    const double2* anp = p.aqsn + static_cast<size_t>(p.band0 + b0) * p.ncouls + igc;
     if (item_regular)
-      sacc_band_loop<NW, IGP_T, COUNT, true>(anp, p.ncouls, nb, s_an, s_am, s_wx, wtr, wti2, qn,
-                                             S1, S2, Sf, cnt);
+      sacc_band_loop<NW, IGP_T, COUNT, true>(anp, p.ncouls, nb, s_an, s_am, wxt, b0 * NW, wtr,
+                                             wti2, qn, S1, S2, Sf, cnt);
     else
-      sacc_band_loop<NW, IGP_T, COUNT, false>(anp, p.ncouls, nb, s_an, s_am, s_wx, wtr, wti2, qn,
-                                              S1, S2, Sf, cnt);
+      sacc_band_loop<NW, IGP_T, COUNT, false>(anp, p.ncouls, nb, s_an, s_am, wxt, b0 * NW, wtr,
+                                              wti2, qn, S1, S2, Sf, cnt);
 
     // Item epilogue: apply the (ig, igp) constants once.
     double a[4 * NW];
@@ -828,15 +876,40 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const Params p) {
     for (int k = 0; k < 4 * NW; ++k) s_acc[k][tid] = a[k];
   }
 
-  Acc<NW> acc;
+  // CTA reduction straight from s_acc (no extra shared scratch, so a 256-band
+  // chunk fits the 48 KB static limit): warp w sums rows w, w + 8, ... in a
+  // fixed order -- eight strided elements per lane, then an xor tree.
+  __syncthreads();
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int k = warp; k < 4 * NW; k += kThreads / 32) {
+    double v = 0.0;
 #pragma unroll
-  for (int iw = 0; iw < NW; ++iw) {
-    acc.a[iw] = make_double2(s_acc[4 * iw + 0][tid], s_acc[4 * iw + 1][tid]);
-    acc.b[iw] = make_double2(s_acc[4 * iw + 2][tid], s_acc[4 * iw + 3][tid]);
+    for (int i = 0; i < kThreads / 32; ++i) v += s_acc[k][lane + 32 * i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) p.partials[static_cast<size_t>(blockIdx.x) * (4 * NW) + k] = v;
   }
-  acc.nn = cnt.nn;
-  acc.nf = cnt.nf;
-  block_reduce_write<NW, COUNT>(acc, p.partials, p.cpartials, 1ull);
+  if constexpr (COUNT) {
+    // The aqsntemp ring is idle now: reuse it for the per-warp counts.
+    unsigned long long* s_cnt = reinterpret_cast<unsigned long long*>(&s_an[0][0]);
+    unsigned long long cn = cnt.nn, cf = cnt.nf;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      cn += __shfl_xor_sync(0xffffffffu, cn, off);
+      cf += __shfl_xor_sync(0xffffffffu, cf, off);
+    }
+    if (lane == 0) {
+      s_cnt[2 * warp] = cn;
+      s_cnt[2 * warp + 1] = cf;
+    }
+    __syncthreads();
+    if (tid < 2) {
+      unsigned long long sum = 0;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) sum += s_cnt[2 * w + tid];
+      p.cpartials[static_cast<size_t>(blockIdx.x) * 2 + tid] = sum;
+    }
+  }
 }
 
 // Sum the per-CTA partials in a fixed order and form achtemp/asxtemp for the

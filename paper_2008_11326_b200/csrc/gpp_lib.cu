@@ -160,6 +160,15 @@ struct Plan {
 };
 
 using KernelFn = void (*)(gpp::Params);
+// The production kernel also takes its band window's wx as a by-value table.
+using SaccFn = void (*)(gpp::Params, gpp::WxTable);
+struct KernelRef {
+  KernelFn fn = nullptr;
+  SaccFn sacc = nullptr;
+  const void* ptr() const {
+    return fn ? reinterpret_cast<const void*>(fn) : reinterpret_cast<const void*>(sacc);
+  }
+};
 
 // Launch-shape override for experiments: GPP_TUNE="igp,bps" forces the igp
 // tile (2..4) of the rcp_sq kernels at nw 2/3 and caps resident CTAs per SM.
@@ -221,32 +230,36 @@ KernelFn pick_plain(int nw) {
 int sacc_igp(int nw) { return nw <= 1 ? 4 : (nw == 2 ? 3 : (nw == 3 ? 2 : 3)); }
 
 template <bool C>
-KernelFn pick_sacc(int nw) {
+KernelRef pick_sacc(int nw) {
+  KernelRef k;
   switch (nw) {
-    case 1: return gpp::gpp_sacc_kernel<1, 4, C>;
-    case 2: return gpp::gpp_sacc_kernel<2, 3, C>;
-    case 3: return gpp::gpp_sacc_kernel<3, 2, C>;
-    default: return gpp::gpp_main_kernel<gpp::FastPolicy, 4, 3, C>;
+    case 1: k.sacc = gpp::gpp_sacc_kernel<1, 4, C>; break;
+    case 2: k.sacc = gpp::gpp_sacc_kernel<2, 3, C>; break;
+    case 3: k.sacc = gpp::gpp_sacc_kernel<3, 2, C>; break;
+    default: k.fn = gpp::gpp_main_kernel<gpp::FastPolicy, 4, 3, C>; break;
   }
+  return k;
 }
 
 template <bool C>
-KernelFn pick_kernel_c(int variant, int nw, int igp_t) {
+KernelRef pick_kernel_c(int variant, int nw, int igp_t) {
+  KernelRef k;
   switch (variant) {
-    case GPP_VARIANT_DIV: return pick_plain<gpp::PlainPolicy<0>, C>(nw);
-    case GPP_VARIANT_RCP: return pick_plain<gpp::PlainPolicy<1>, C>(nw);
-    case GPP_KERNEL_SQ_SPLIT: return pick_fast_nw<gpp::FastPolicyT<0, 2>, C>(nw, igp_t);
-    case GPP_KERNEL_IW_HOIST: return pick_fast_nw<gpp::FastPolicyT<1, 3>, C>(nw, igp_t);
-    case GPP_KERNEL_ONE_SEED: return pick_fast_nw<gpp::FastPolicy, C>(nw, igp_t);
-    default: return pick_sacc<C>(nw);
+    case GPP_VARIANT_DIV: k.fn = pick_plain<gpp::PlainPolicy<0>, C>(nw); break;
+    case GPP_VARIANT_RCP: k.fn = pick_plain<gpp::PlainPolicy<1>, C>(nw); break;
+    case GPP_KERNEL_SQ_SPLIT: k.fn = pick_fast_nw<gpp::FastPolicyT<0, 2>, C>(nw, igp_t); break;
+    case GPP_KERNEL_IW_HOIST: k.fn = pick_fast_nw<gpp::FastPolicyT<1, 3>, C>(nw, igp_t); break;
+    case GPP_KERNEL_ONE_SEED: k.fn = pick_fast_nw<gpp::FastPolicy, C>(nw, igp_t); break;
+    default: k = pick_sacc<C>(nw); break;
   }
+  return k;
 }
 
 // count: whether the kernel also produces the near/far branch counts (the
 // reference's branch_stats, kernel.py:130-137).  The uncounted kernel is the
 // evaluate_variant path; the counted one costs two predicated integer adds
 // per instance.
-KernelFn pick_kernel(int variant, int nw, int igp_t, bool count) {
+KernelRef pick_kernel(int variant, int nw, int igp_t, bool count) {
   return count ? pick_kernel_c<true>(variant, nw, igp_t) : pick_kernel_c<false>(variant, nw, igp_t);
 }
 
@@ -277,11 +290,12 @@ int choose_igp_tile(int64_t ngpown) {
 // measured at ~4 bands' worth of work (tools/probe_shard.py: step time of
 // 1/N band shards).  Long chunks amortise that cost; short ones balance
 // small shards (and small ig slabs) across the 148 SMs.
-int choose_bchunk(long long n_igblk, long long n_igptile, int64_t nbands, long long slots) {
+int choose_bchunk(long long n_igblk, long long n_igptile, int64_t nbands, long long slots,
+                  int max_chunk) {
   constexpr double kItemOverheadBands = 4.0;
   int bchunk = 8;
   double best = -1.0;
-  for (int bc = 8; bc <= gpp::kMaxChunk; bc *= 2) {
+  for (int bc = 8; bc <= max_chunk; bc *= 2) {
     const int eff = static_cast<int>(std::min<int64_t>(bc, nbands));
     const long long items = n_igblk * n_igptile * ((nbands + eff - 1) / eff);
     const long long waves = (items + slots - 1) / slots;
@@ -309,16 +323,17 @@ int make_plan_uncached(gpp_ctx* c, int variant, int nw_group, bool count, Plan* 
                                                                   : choose_igp_tile(c->ngpown));
   pl->n_igblk = static_cast<int>((c->ncouls + gpp::kThreads - 1) / gpp::kThreads);
   pl->n_igptile = static_cast<int>((c->ngpown + pl->igp_t - 1) / pl->igp_t);
-  KernelFn fn = pick_kernel(variant, nw_group, pl->igp_t, count);
+  const KernelRef fn = pick_kernel(variant, nw_group, pl->igp_t, count);
   int bps = 0;
-  GPP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, gpp::kThreads, 0));
+  GPP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn.ptr(), gpp::kThreads, 0));
   cudaFuncAttributes attr;
-  GPP_CUDA(cudaFuncGetAttributes(&attr, fn));
+  GPP_CUDA(cudaFuncGetAttributes(&attr, fn.ptr()));
   pl->regs = attr.numRegs;
   pl->blocks_per_sm = std::max(bps, 1);
   if (tune.bps > 0) pl->blocks_per_sm = std::min(pl->blocks_per_sm, tune.bps);
   const long long slots = static_cast<long long>(pl->blocks_per_sm) * c->num_sms;
-  const int bchunk = choose_bchunk(pl->n_igblk, pl->n_igptile, c->nbands, slots);
+  const int bchunk = choose_bchunk(pl->n_igblk, pl->n_igptile, c->nbands, slots,
+                                   fn.sacc ? gpp::kSaccChunk : gpp::kMaxChunk);
   pl->bchunk = bchunk;
   pl->n_items = static_cast<long long>(pl->n_igblk) * pl->n_igptile *
                 ((c->nbands + bchunk - 1) / bchunk);
@@ -383,9 +398,17 @@ int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool
     Plan pl;
     int rc = make_plan(c, variant, nwg, count, &pl);
     if (rc) return rc;
-    GPP_CUDA(c->partials.ensure(static_cast<size_t>(pl.grid) * n_slabs * 4 * gpp::kMaxNwGroup));
-    GPP_CUDA(c->cpartials.ensure(static_cast<size_t>(pl.grid) * n_slabs * 2));
-    KernelFn fn = pick_kernel(variant, nwg, pl.igp_t, count);
+    const KernelRef fn = pick_kernel(variant, nwg, pl.igp_t, count);
+    // The production kernel reads wx from a by-value table, so it runs one
+    // launch per band window of at most kWxParam / nwg bands (one window up
+    // to 512 bands at three frequencies); the other kernels take all bands.
+    const int64_t win = fn.sacc ? gpp::kWxParam / nwg : c->nbands;
+    const int n_win = static_cast<int>((c->nbands + win - 1) / win);
+    if (fn.sacc && pl.n_items >= (1ll << 31))
+      return fail(GPP_ERR_ARG, "too many work items for one launch");
+    GPP_CUDA(c->partials.ensure(static_cast<size_t>(pl.grid) * n_slabs * n_win * 4 *
+                                gpp::kMaxNwGroup));
+    GPP_CUDA(c->cpartials.ensure(static_cast<size_t>(pl.grid) * n_slabs * n_win * 2));
     int rows = 0;  // partial rows written by this frequency group
     if (ev_main && gi == 0) GPP_CUDA(cudaEventRecord(ev_main[0], c->stream));
     // Slabs alternate between two streams so that slab s+1's CTAs fill the
@@ -401,35 +424,50 @@ int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool
       if (nblk <= 0) continue;
       cudaStream_t ks = (two && (s & 1)) ? c->kstream2 : c->stream;
       if (gi == 0 && !sl.ready.empty()) GPP_CUDA(cudaStreamWaitEvent(ks, sl.ready[s], 0));
-      gpp::Params p;
-      p.wtilde = c->wtilde.ptr;
-      p.eps = c->eps.ptr;
-      p.aqsn = c->aqsn.ptr;
-      p.aqsm = c->aqsm.ptr;
-      p.wxb = c->wxb.ptr;
-      p.ncouls = static_cast<int>(c->ncouls);
-      p.ngpown = static_cast<int>(c->ngpown);
-      p.nbands = static_cast<int>(c->nbands);
-      p.nw_total = c->nw;
-      p.iw0 = iw0;
-      p.igblk0 = sl.blk0[s];
-      p.n_igblk = nblk;
-      p.n_igptile = pl.n_igptile;
-      // A slab re-plans its band chunk for its own item count: short chunks
-      // keep the last (small) slabs from idling most of the SMs.
-      p.bchunk = nblk == pl.n_igblk
-                     ? pl.bchunk
-                     : choose_bchunk(nblk, pl.n_igptile, c->nbands,
-                                     static_cast<long long>(pl.blocks_per_sm) * c->num_sms);
-      p.n_items = static_cast<long long>(nblk) * pl.n_igptile *
-                  ((c->nbands + p.bchunk - 1) / p.bchunk);
-      p.wxmax = c->wxmax;
-      const int grid = static_cast<int>(std::min<long long>(pl.grid, p.n_items));
-      p.partials = c->partials.ptr + static_cast<size_t>(rows) * 4 * nwg;
-      p.cpartials = c->cpartials.ptr + static_cast<size_t>(rows) * 2;
-      fn<<<grid, gpp::kThreads, 0, ks>>>(p);
-      GPP_CUDA(cudaGetLastError());
-      rows += grid;
+      for (int w = 0; w < n_win; ++w) {
+        const int64_t wb0 = w * win, wnb = std::min<int64_t>(win, c->nbands - wb0);
+        gpp::Params p;
+        p.wtilde = c->wtilde.ptr;
+        p.eps = c->eps.ptr;
+        p.aqsn = c->aqsn.ptr;
+        p.aqsm = c->aqsm.ptr;
+        p.wxb = c->wxb.ptr;
+        p.ncouls = static_cast<int>(c->ncouls);
+        p.ngpown = static_cast<int>(c->ngpown);
+        p.nbands = static_cast<int>(wnb);
+        p.band0 = static_cast<int>(wb0);
+        p.nw_total = c->nw;
+        p.iw0 = iw0;
+        p.igblk0 = sl.blk0[s];
+        p.n_igblk = nblk;
+        p.n_igptile = pl.n_igptile;
+        gpp::fastdiv_init(static_cast<unsigned>(p.n_igptile), &p.igpt_mul, &p.igpt_shift);
+        gpp::fastdiv_init(static_cast<unsigned>(p.n_igblk), &p.igblk_mul, &p.igblk_shift);
+        // A slab (or band window) re-plans its band chunk for its own item
+        // count: short chunks keep the last (small) slabs from idling most of
+        // the SMs.
+        p.bchunk = (nblk == pl.n_igblk && wnb == c->nbands)
+                       ? pl.bchunk
+                       : choose_bchunk(nblk, pl.n_igptile, wnb,
+                                       static_cast<long long>(pl.blocks_per_sm) * c->num_sms,
+                                       fn.sacc ? gpp::kSaccChunk : gpp::kMaxChunk);
+        p.n_items = static_cast<long long>(nblk) * pl.n_igptile * ((wnb + p.bchunk - 1) / p.bchunk);
+        p.wxmax = c->wxmax;
+        const int grid = static_cast<int>(std::min<long long>(pl.grid, p.n_items));
+        p.partials = c->partials.ptr + static_cast<size_t>(rows) * 4 * nwg;
+        p.cpartials = c->cpartials.ptr + static_cast<size_t>(rows) * 2;
+        if (fn.sacc) {
+          gpp::WxTable t;
+          for (int64_t b = 0; b < wnb; ++b)
+            for (int iw = 0; iw < nwg; ++iw)
+              t.w[b * nwg + iw] = c->h_wx[(wb0 + b) * c->nw + iw0 + iw];
+          fn.sacc<<<grid, gpp::kThreads, 0, ks>>>(p, t);
+        } else {
+          fn.fn<<<grid, gpp::kThreads, 0, ks>>>(p);
+        }
+        GPP_CUDA(cudaGetLastError());
+        rows += grid;
+      }
     }
     if (two) {
       GPP_CUDA(cudaEventRecord(c->ev_join, c->kstream2));
