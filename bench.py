@@ -458,16 +458,25 @@ def run_ours(args, dist: Dist):
         ceil = peak_tf * (1 + prof["fma_ratio"]) / 2
         line["fma_ceiling_tflops_executed_mix"] = ceil
         line["pct_fma_ceiling_ncu_counted"] = 100.0 * ex / ceil
+        # the kernel executes fewer FP64 operations than the
+        # reference's analytic count (per-instance algebra: one rsqrt seed for
+        # 1/d and sqrt(d), (ig, igp) constants applied once per item), so the
+        # algorithmic rate is an EFFECTIVE rate.  The hardware utilisation is
+        # the ncu-counted fraction beside it.
+        line["roofline"]["achieved_kind"] = (
+            "effective: the reference's analytic FLOPs (kernel.py:191-212) per launch / kernel time; "
+            f"the kernel executes {100.0 * prof['executed_over_algorithmic']:.0f}% of them (ncu)")
+        line["roofline"]["achieved_executed"] = ex
+        line["roofline"]["frac_executed"] = ex / peak_tf
     from paper_2008_11326_b200.counters import BranchStats, counters_from_stats, fma_ratio
 
     cnt = counters_from_stats("rcp_sq", BranchStats(tot_inst, near, far), nb * ng * nc, True)
     r = fma_ratio(cnt)
     line["roofline"]["fma_ratio_analytic"] = r
-    # The paper's FMA-ratio ceiling with the reference's analytic instruction
-    # mix (kernel.py:144-212): what the algorithmic FLOPs could reach if the
-    # machine executed exactly the reference's counted instructions.
+    # The paper's FMA-ratio ceiling for the reference's analytic instruction
+    # mix (kernel.py:144-212).  It bounds EXECUTED FLOPs of that mix; the
+    # effective rate above is not compared with it (it can exceed it).
     line["fma_ceiling_tflops_analytic_mix"] = peak_tf * (1 + r) / 2
-    line["pct_fma_ceiling_analytic_mix"] = 100.0 * value / dist.world / line["fma_ceiling_tflops_analytic_mix"]
     if args.variant == "rcp_sq":
         line["parity"] = golden_parity(result, args.workload, args.seed, args.nw)
     print(json.dumps(line), flush=True)

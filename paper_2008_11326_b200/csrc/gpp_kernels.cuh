@@ -662,6 +662,16 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_main_kernel(const Params p) {
 // per-thread ach/asx accumulators live in shared memory (updated once per
 // item) to leave the registers to the S sums.
 // ---------------------------------------------------------------------------
+// First kAnDepth - 1 bands of an item's aqsntemp ring, one commit group each.
+__device__ __forceinline__ void sacc_prefill(const double2* anp, int ncouls, int nb,
+                                             double2 (&s_an)[kAnDepth][kThreads]) {
+#pragma unroll
+  for (int s = 0; s < kAnDepth - 1; ++s) {
+    if (s < nb) cp_async16(&s_an[s][threadIdx.x], anp + static_cast<size_t>(s) * ncouls);
+    cp_async_commit();
+  }
+}
+
 template <int NW, int IGP_T, bool COUNT, bool FAST>
 __device__ __forceinline__ void sacc_band_loop(const double2* anp, int ncouls, int nb,
                                                double2 (&s_an)[kAnDepth][kThreads],
@@ -673,12 +683,8 @@ __device__ __forceinline__ void sacc_band_loop(const double2* anp, int ncouls, i
                                                double2 (&S1)[IGP_T][NW], double2 (&S2)[IGP_T][NW],
                                                double2 (&Sf)[IGP_T][NW], Acc<1>& cnt) {
   const int tid = threadIdx.x;
-#pragma unroll
-  for (int s = 0; s < kAnDepth - 1; ++s) {
-    if (s < nb) cp_async16(&s_an[s][tid], anp + static_cast<size_t>(s) * ncouls);
-    cp_async_commit();
-  }
-  // Prefetch address advanced incrementally (one 64-bit add per band, not a
+  // (The ring's first kAnDepth - 1 bands were issued by the item prologue,
+  // sacc_prefill.)  Prefetch address advanced incrementally (one 64-bit add per band, not a
   // wide multiply): four fewer integer instructions in the band loop.
   const double2* pfp = anp + static_cast<size_t>(kAnDepth - 1) * ncouls;
   for (int bb = 0; bb < nb; ++bb) {
@@ -710,7 +716,17 @@ __device__ __forceinline__ void sacc_band_loop(const double2* anp, int ncouls, i
         double in, gf;
         if constexpr (FAST && !COUNT) {
           // One rsqrt seed, one cubic step: 1/d = rr^2, sqrt(d) = t (1 + q).
-          const double r = rsqrt_approx(d);
+          // MUFU.RSQ64H writes only the high word; pair it with the (dead)
+          // low word of wdre instead of a zeroed register.  The low word
+          // perturbs the 2^-20 seed by < 2^-20 relative, which the cubic step
+          // absorbs (its error is O(e^3)).
+          double r;
+          asm("{\n\t.reg .b32 wl, wh, rl, rh;\n\t.reg .f64 s;\n\t"
+              "mov.b64 {wl, wh}, %1;\n\t"
+              "rsqrt.approx.ftz.f64 s, %2;\n\t"
+              "mov.b64 {rl, rh}, s;\n\t"
+              "mov.b64 %0, {wl, rh};\n\t}"
+              : "=d"(r) : "d"(wdre), "d"(d));
           const double t = d * r;
           const double e = fma(-t, r, 1.0);
           const double pe = fma(e, 0.375, 0.5);
@@ -781,7 +797,7 @@ __device__ __forceinline__ void sacc_band_loop(const double2* anp, int ncouls, i
 template <int NW, int IGP_T, bool COUNT>
 __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_constant__ Params p,
                                                                const __grid_constant__ WxTable wxt) {
-  __shared__ double2 s_am[kSaccChunk][IGP_T];
+  __shared__ __align__(16) double2 s_am[kSaccChunk][IGP_T];
   __shared__ __align__(16) double2 s_an[kAnDepth][kThreads];
   __shared__ double s_acc[4 * NW][kThreads];  // this thread's ach/asx partials
   const int tid = threadIdx.x;
@@ -804,6 +820,24 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
     const int b0 = bc * p.bchunk;
     const int nb = min(p.bchunk, p.nbands - b0);
 
+    const double2* anp = p.aqsn + static_cast<size_t>(p.band0 + b0) * p.ncouls + igc;
+
+    // Item prologue: the aqsmtemp tile (-> shared), the first aqsntemp ring
+    // bands and wtilde are independent loads, so all three are in flight at
+    // once instead of three exposed latencies in a row.  The barrier first
+    // retires the previous item's reads of s_am.
+    __syncthreads();
+    for (int k = tid; k < nb * IGP_T; k += kThreads) {
+      const int bb = k / IGP_T, j = k - bb * IGP_T;
+      const int igp = igpt * IGP_T + j;
+      if (igp < p.ngpown)
+        cp_async16(&s_am[bb][j], p.aqsm + static_cast<size_t>(p.band0 + b0 + bb) * p.ngpown + igp);
+      else
+        s_am[bb][j] = make_double2(0.0, 0.0);
+    }
+    cp_async_commit();
+    sacc_prefill(anp, p.ncouls, nb, s_an);
+
     double wtr[IGP_T], wti2[IGP_T], qn[IGP_T];
     bool thread_regular = true;
 #pragma unroll
@@ -820,15 +854,8 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
       const double m = p.wxmax + sqrt(wt2);
       thread_regular = thread_regular && (!v || (wt.y != 0.0 && wt2 > 1.000001e-24 * m * m));
     }
+    cp_async_wait<kAnDepth - 1>();  // this thread's s_am copies (the ring may still fly)
     const bool item_regular = __syncthreads_and(!COUNT && thread_regular) != 0;
-    for (int k = tid; k < nb * IGP_T; k += kThreads) {
-      const int bb = k / IGP_T, j = k - bb * IGP_T;
-      const int igp = igpt * IGP_T + j;
-      s_am[bb][j] = igp < p.ngpown
-                        ? __ldg(p.aqsm + static_cast<size_t>(p.band0 + b0 + bb) * p.ngpown + igp)
-                        : make_double2(0.0, 0.0);
-    }
-    __syncthreads();
 
     double2 S1[IGP_T][NW], S2[IGP_T][NW], Sf[IGP_T][NW];
 #pragma unroll
@@ -839,7 +866,6 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
         S2[j][iw] = make_double2(0.0, 0.0);
         Sf[j][iw] = make_double2(0.0, 0.0);
       }
-    const double2* anp = p.aqsn + static_cast<size_t>(p.band0 + b0) * p.ncouls + igc;
     if (item_regular)
       sacc_band_loop<NW, IGP_T, COUNT, true>(anp, p.ncouls, nb, s_an, s_am, wxt, b0 * NW, wtr,
                                              wti2, qn, S1, S2, Sf, cnt);
