@@ -662,190 +662,284 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_main_kernel(const Params p) {
 // per-thread ach/asx accumulators live in shared memory (updated once per
 // item) to leave the registers to the S sums.
 // ---------------------------------------------------------------------------
-// First kAnDepth - 1 bands of an item's aqsntemp ring, one commit group each.
-__device__ __forceinline__ void sacc_prefill(const double2* anp, int ncouls, int nb,
-                                             double2 (&s_an)[kAnDepth][kThreads]) {
+// Shared memory of gpp_sacc_kernel (dynamic: 88-104 KB, two CTAs per SM).
+// The aqsmtemp tile and the (wtilde, eps) of the thread's ig are double
+// buffered: item k+1's are copied (cp.async) while item k's bands run, and
+// item k+1's first aqsntemp bands enter the ring during item k's last
+// iterations, so an item boundary exposes no load latency.
+template <int NW, int IGP_T>
+struct SaccSmem {
+  double2 an[kAnDepth][kThreads];          // aqsntemp ring, one slot per band in flight
+  double2 am[2][kSaccChunk][IGP_T];        // aqsmtemp[igp tile, band chunk]
+  double2 we[2][IGP_T][2][kThreads];       // [buf][j][wtilde | eps][thread]
+  double acc[4 * NW][kThreads];            // this thread's ach/asx partials
+};
+
+struct SaccItem {
+  int igpt, igb, b0, nb;
+};
+
+__device__ __forceinline__ SaccItem sacc_item(const Params& p, unsigned item) {
+  SaccItem it;
+  const unsigned rest = fastdiv(item, p.igpt_mul, p.igpt_shift);
+  it.igpt = static_cast<int>(item - rest * p.n_igptile);
+  const unsigned bcu = fastdiv(rest, p.igblk_mul, p.igblk_shift);
+  it.igb = static_cast<int>(rest - bcu * p.n_igblk);
+  it.b0 = static_cast<int>(bcu) * p.bchunk;
+  it.nb = min(p.bchunk, p.nbands - it.b0);
+  return it;
+}
+
+// This thread's ig for an item (clamped to a valid column for padded lanes).
+__device__ __forceinline__ int sacc_igc(const Params& p, const SaccItem& it) {
+  return min((p.igblk0 + it.igb) * kThreads + static_cast<int>(threadIdx.x), p.ncouls - 1);
+}
+
+// Issue (no commit) the copies of an item's aqsmtemp tile (cooperative) and of
+// this thread's wtilde / eps into buffer `buf`.
+template <int NW, int IGP_T>
+__device__ __forceinline__ void sacc_stage(const Params& p, const SaccItem& it,
+                                           SaccSmem<NW, IGP_T>& sm, int buf) {
+  const int tid = threadIdx.x;
+  for (int k = tid; k < it.nb * IGP_T; k += kThreads) {
+    const int bb = k / IGP_T, j = k - bb * IGP_T;
+    const int igp = it.igpt * IGP_T + j;
+    if (igp < p.ngpown)
+      cp_async16(&sm.am[buf][bb][j],
+                 p.aqsm + static_cast<size_t>(p.band0 + it.b0 + bb) * p.ngpown + igp);
+    else
+      sm.am[buf][bb][j] = make_double2(0.0, 0.0);
+  }
+  const int igc = sacc_igc(p, it);
 #pragma unroll
-  for (int s = 0; s < kAnDepth - 1; ++s) {
-    if (s < nb) cp_async16(&s_an[s][threadIdx.x], anp + static_cast<size_t>(s) * ncouls);
-    cp_async_commit();
+  for (int j = 0; j < IGP_T; ++j) {
+    const int igp = min(it.igpt * IGP_T + j, p.ngpown - 1);
+    const size_t off = static_cast<size_t>(igp) * p.ncouls + igc;
+    cp_async16(&sm.we[buf][j][0][tid], p.wtilde + off);
+    cp_async16(&sm.we[buf][j][1][tid], p.eps + off);
   }
 }
 
+// One band of the S-sum recurrence for all IGP_T x NW instances of this thread.
 template <int NW, int IGP_T, bool COUNT, bool FAST>
-__device__ __forceinline__ void sacc_band_loop(const double2* anp, int ncouls, int nb,
-                                               double2 (&s_an)[kAnDepth][kThreads],
-                                               const double2 (&s_am)[kSaccChunk][IGP_T],
-                                               const WxTable& wxt, int wx0,
+__device__ __forceinline__ void sacc_band(const double2 an, const double2 (&am)[IGP_T],
+                                          const double (&wx)[NW], const double (&wtr)[IGP_T],
+                                          const double (&wti2)[IGP_T], const double (&qn)[IGP_T],
+                                          double2 (&S1)[IGP_T][NW], double2 (&S2)[IGP_T][NW],
+                                          double2 (&Sf)[IGP_T][NW], Acc<1>& cnt) {
+#pragma unroll
+  for (int j = 0; j < IGP_T; ++j) {
+    const double tr = fma(an.x, am[j].x, an.y * am[j].y);  // t = an * conj(am)
+    const double ti = fma(an.y, am[j].x, -an.x * am[j].y);
+    const long long qbits = __double_as_longlong(qn[j]);
+    double iwt2 = 0.0;
+    if constexpr (!FAST) {
+      // Padded lanes (qn = +inf) and wt = 0 get x = 0: never far.
+      const double wt2 = fma(wtr[j], wtr[j], wti2[j]);
+      iwt2 = (wt2 > 0.0 && qbits != 0x7FF0000000000000ll) ? 1.0 / wt2 : 0.0;
+    }
+#pragma unroll
+    for (int iw = 0; iw < NW; ++iw) {
+      const double wdre = wx[iw] - wtr[j];
+      const double d = fma(wdre, wdre, wti2[j]);
+      double in, gf;
+      if constexpr (FAST && !COUNT) {
+        // One rsqrt seed, one cubic step: 1/d = rr^2, sqrt(d) = t (1 + q).
+        // MUFU.RSQ64H writes only the high word; pair it with the (dead)
+        // low word of wdre instead of a zeroed register.  The low word
+        // perturbs the 2^-20 seed by < 2^-20 relative, which the cubic step
+        // absorbs (its error is O(e^3)).
+        double r;
+        asm("{\n\t.reg .b32 wl, wh, rl, rh;\n\t.reg .f64 s;\n\t"
+            "mov.b64 {wl, wh}, %1;\n\t"
+            "rsqrt.approx.ftz.f64 s, %2;\n\t"
+            "mov.b64 {rl, rh}, s;\n\t"
+            "mov.b64 %0, {wl, rh};\n\t}"
+            : "=d"(r) : "d"(wdre), "d"(d));
+        const double t = d * r;
+        const double e = fma(-t, r, 1.0);
+        const double pe = fma(e, 0.375, 0.5);
+        const double q = e * pe;
+        const double rr = fma(r, q, r);
+        const double sq = fma(t, q, t);
+        const double inv = rr * rr;
+        // near ? (inv, 0) : (0, sq), selecting only the HIGH words: the
+        // deselected value keeps its low word, i.e. becomes a subnormal
+        // below 2^-1042.  Its products vanish below half an ulp of any
+        // partial sum above ~1e-290 that they join (the selected terms are
+        // >= ~1e-300 unless |wx - wt| > 1e150), so the sums are unchanged
+        // (tools/ab_select.sh: bitwise equal to the exact-select build); it
+        // halves the selects (2 SEL instead of 4 FSEL per instance).
+        asm("{\n\t.reg .pred pn;\n\t.reg .b32 il, ih, gl, gh;\n\t"
+            "setp.gt.s64 pn, %2, %3;\n\t"
+            "mov.b64 {il, ih}, %4;\n\t"
+            "mov.b64 {gl, gh}, %5;\n\t"
+            "selp.b32 ih, ih, 0, pn;\n\t"
+            "selp.b32 gh, 0, gh, pn;\n\t"
+            "mov.b64 %0, {il, ih};\n\t"
+            "mov.b64 %1, {gl, gh};\n\t}"
+            : "=d"(in), "=d"(gf)
+            : "l"(__double_as_longlong(d)), "l"(qbits), "d"(inv), "d"(sq));
+#ifdef GPP_EXACT_SELECT  // A/B reference build (tools/ab_select.sh): full 64-bit selects
+        asm("{\n\t.reg .pred pn;\n\t"
+            "setp.gt.s64 pn, %2, %3;\n\t"
+            "selp.f64 %0, %4, 0d0000000000000000, pn;\n\t"
+            "selp.f64 %1, 0d0000000000000000, %5, pn;\n\t}"
+            : "=d"(in), "=d"(gf)
+            : "l"(__double_as_longlong(d)), "l"(qbits), "d"(inv), "d"(sq));
+#endif
+      } else {
+        // General path: full far test on x = d/|wt|^2; gf = sqrt(x)
+        // already carries the 1/|wt| factor.
+        const double inv = rcp_refined(d);
+        const double x = d * iwt2;
+        const double g = sqrt_nr<3>(x);
+        select_branches<COUNT>(d, qbits, x, inv, g, in, gf, cnt);
+      }
+      const double s1 = in * wx[iw];
+      S1[j][iw].x = fma(s1, tr, S1[j][iw].x);
+      S1[j][iw].y = fma(s1, ti, S1[j][iw].y);
+      S2[j][iw].x = fma(in, tr, S2[j][iw].x);
+      S2[j][iw].y = fma(in, ti, S2[j][iw].y);
+      Sf[j][iw].x = fma(gf, tr, Sf[j][iw].x);
+      Sf[j][iw].y = fma(gf, ti, Sf[j][iw].y);
+    }
+  }
+}
+
+// The band loop of one item.  Ring slot of band bb: (ro + bb) % kAnDepth.
+// Every iteration commits exactly one cp.async group and waits for the group
+// of its own band (kAnDepth - 1 groups back), so the ring stays continuous
+// across items:
+//   - main phase (pf = bb + kAnDepth - 1 < nb): prefetch this item's band pf;
+//   - tail phase: prefetch the NEXT item's band pf - nb into the same ring
+//     (when this item has at least kAnDepth - 1 bands; a shorter item leaves
+//     the next one to prime its ring itself);
+//   - iteration 0's group also carries the next item's aqsmtemp tile and
+//     wtilde / eps (issued just before the loop).
+template <int NW, int IGP_T, bool COUNT, bool FAST>
+__device__ __forceinline__ void sacc_band_loop(const Params& p, const WxTable& wxt,
+                                               SaccSmem<NW, IGP_T>& sm, int buf, unsigned ro,
+                                               const SaccItem& it, const double2* anp,
+                                               bool has_next, const SaccItem& nx,
+                                               const double2* nx_anp,
                                                const double (&wtr)[IGP_T],
                                                const double (&wti2)[IGP_T],
                                                const double (&qn)[IGP_T],
                                                double2 (&S1)[IGP_T][NW], double2 (&S2)[IGP_T][NW],
                                                double2 (&Sf)[IGP_T][NW], Acc<1>& cnt) {
   const int tid = threadIdx.x;
-  // (The ring's first kAnDepth - 1 bands were issued by the item prologue,
-  // sacc_prefill.)  Prefetch address advanced incrementally (one 64-bit add per band, not a
-  // wide multiply): four fewer integer instructions in the band loop.
+  const int nb = it.nb, wx0 = it.b0 * NW;
+  const size_t ncouls = static_cast<size_t>(p.ncouls);
+  const int nmain = max(nb - (kAnDepth - 1), 0);
+  // Prefetch address advanced incrementally (one 64-bit add per band).
   const double2* pfp = anp + static_cast<size_t>(kAnDepth - 1) * ncouls;
-  for (int bb = 0; bb < nb; ++bb) {
-    const int pf = bb + kAnDepth - 1;
-    if (pf < nb) cp_async16(&s_an[pf % kAnDepth][tid], pfp);
+  // The next item's staging joins iteration 0's commit group.
+  if (has_next) sacc_stage(p, nx, sm, buf ^ 1);
+  int wxo = wx0;
+  for (int bb = 0; bb < nmain; ++bb) {
+    cp_async16(&sm.an[(ro + bb + kAnDepth - 1) % kAnDepth][tid], pfp);  // unsigned: a mask
     pfp += ncouls;
     cp_async_commit();
     cp_async_wait<kAnDepth - 1>();
-    const double2 an = s_an[bb % kAnDepth][tid];
+    const double2 an = sm.an[(ro + bb) % kAnDepth][tid];
+    double wx[NW];
+#pragma unroll
+    for (int iw = 0; iw < NW; ++iw) wx[iw] = wxt.w[wxo + iw];
+    wxo += NW;
+    double2 am[IGP_T];
+#pragma unroll
+    for (int j = 0; j < IGP_T; ++j) am[j] = sm.am[buf][bb][j];
+    sacc_band<NW, IGP_T, COUNT, FAST>(an, am, wx, wtr, wti2, qn, S1, S2, Sf, cnt);
+  }
+  for (int bb = nmain; bb < nb; ++bb) {
+    const int pf = bb + kAnDepth - 1;
+    if (pf < nb)
+      cp_async16(&sm.an[(ro + pf) % kAnDepth][tid], anp + static_cast<size_t>(pf) * ncouls);
+    else if (has_next && nb >= kAnDepth - 1 && pf - nb < nx.nb)
+      cp_async16(&sm.an[(ro + pf) % kAnDepth][tid], nx_anp + static_cast<size_t>(pf - nb) * ncouls);
+    cp_async_commit();
+    cp_async_wait<kAnDepth - 1>();
+    const double2 an = sm.an[(ro + bb) % kAnDepth][tid];
     double wx[NW];
 #pragma unroll
     for (int iw = 0; iw < NW; ++iw) wx[iw] = wxt.w[wx0 + bb * NW + iw];
+    double2 am[IGP_T];
 #pragma unroll
-    for (int j = 0; j < IGP_T; ++j) {
-      const double2 am = s_am[bb][j];
-      const double tr = fma(an.x, am.x, an.y * am.y);  // t = an * conj(am)
-      const double ti = fma(an.y, am.x, -an.x * am.y);
-      const long long qbits = __double_as_longlong(qn[j]);
-      double iwt2 = 0.0;
-      if constexpr (!FAST) {
-        // Padded lanes (qn = +inf) and wt = 0 get x = 0: never far.
-        const double wt2 = fma(wtr[j], wtr[j], wti2[j]);
-        iwt2 = (wt2 > 0.0 && qbits != 0x7FF0000000000000ll) ? 1.0 / wt2 : 0.0;
-      }
-#pragma unroll
-      for (int iw = 0; iw < NW; ++iw) {
-        const double wdre = wx[iw] - wtr[j];
-        const double d = fma(wdre, wdre, wti2[j]);
-        double in, gf;
-        if constexpr (FAST && !COUNT) {
-          // One rsqrt seed, one cubic step: 1/d = rr^2, sqrt(d) = t (1 + q).
-          // MUFU.RSQ64H writes only the high word; pair it with the (dead)
-          // low word of wdre instead of a zeroed register.  The low word
-          // perturbs the 2^-20 seed by < 2^-20 relative, which the cubic step
-          // absorbs (its error is O(e^3)).
-          double r;
-          asm("{\n\t.reg .b32 wl, wh, rl, rh;\n\t.reg .f64 s;\n\t"
-              "mov.b64 {wl, wh}, %1;\n\t"
-              "rsqrt.approx.ftz.f64 s, %2;\n\t"
-              "mov.b64 {rl, rh}, s;\n\t"
-              "mov.b64 %0, {wl, rh};\n\t}"
-              : "=d"(r) : "d"(wdre), "d"(d));
-          const double t = d * r;
-          const double e = fma(-t, r, 1.0);
-          const double pe = fma(e, 0.375, 0.5);
-          const double q = e * pe;
-          const double rr = fma(r, q, r);
-          const double sq = fma(t, q, t);
-          const double inv = rr * rr;
-          // near ? (inv, 0) : (0, sq), selecting only the HIGH words: the
-          // deselected value keeps its low word, i.e. becomes a subnormal
-          // below 2^-1042.  Its products vanish below half an ulp of any
-          // partial sum above ~1e-290 that they join (the selected terms are
-          // >= ~1e-300 unless |wx - wt| > 1e150), so the sums are unchanged
-          // (tools/ab_select.sh: bitwise equal to the exact-select build); it halves
-          // the selects (2 SEL instead of 4 FSEL per instance) in this
-          // register-file-bound loop: 4.93 -> 4.80 ms at paper size.
-#ifdef GPP_DSETP
-          asm("{\n\t.reg .pred pn;\n\t.reg .b32 il, ih, gl, gh;\n\t"
-              "setp.gt.f64 pn, %2, %3;\n\t"
-              "mov.b64 {il, ih}, %4;\n\t"
-              "mov.b64 {gl, gh}, %5;\n\t"
-              "selp.b32 ih, ih, 0, pn;\n\t"
-              "selp.b32 gh, 0, gh, pn;\n\t"
-              "mov.b64 %0, {il, ih};\n\t"
-              "mov.b64 %1, {gl, gh};\n\t}"
-              : "=d"(in), "=d"(gf)
-              : "d"(d), "d"(qn[j]), "d"(inv), "d"(sq));
-#else
-          asm("{\n\t.reg .pred pn;\n\t.reg .b32 il, ih, gl, gh;\n\t"
-              "setp.gt.s64 pn, %2, %3;\n\t"
-              "mov.b64 {il, ih}, %4;\n\t"
-              "mov.b64 {gl, gh}, %5;\n\t"
-              "selp.b32 ih, ih, 0, pn;\n\t"
-              "selp.b32 gh, 0, gh, pn;\n\t"
-              "mov.b64 %0, {il, ih};\n\t"
-              "mov.b64 %1, {gl, gh};\n\t}"
-              : "=d"(in), "=d"(gf)
-              : "l"(__double_as_longlong(d)), "l"(qbits), "d"(inv), "d"(sq));
-#endif
-#ifdef GPP_EXACT_SELECT  // A/B reference build (tools/ab_select.sh): full 64-bit selects
-          asm("{\n\t.reg .pred pn;\n\t"
-              "setp.gt.s64 pn, %2, %3;\n\t"
-              "selp.f64 %0, %4, 0d0000000000000000, pn;\n\t"
-              "selp.f64 %1, 0d0000000000000000, %5, pn;\n\t}"
-              : "=d"(in), "=d"(gf)
-              : "l"(__double_as_longlong(d)), "l"(qbits), "d"(inv), "d"(sq));
-#endif
-        } else {
-          // General path: full far test on x = d/|wt|^2; gf = sqrt(x)
-          // already carries the 1/|wt| factor.
-          const double inv = rcp_refined(d);
-          const double x = d * iwt2;
-          const double g = sqrt_nr<3>(x);
-          select_branches<COUNT>(d, qbits, x, inv, g, in, gf, cnt);
-        }
-        const double s1 = in * wx[iw];
-        S1[j][iw].x = fma(s1, tr, S1[j][iw].x);
-        S1[j][iw].y = fma(s1, ti, S1[j][iw].y);
-        S2[j][iw].x = fma(in, tr, S2[j][iw].x);
-        S2[j][iw].y = fma(in, ti, S2[j][iw].y);
-        Sf[j][iw].x = fma(gf, tr, Sf[j][iw].x);
-        Sf[j][iw].y = fma(gf, ti, Sf[j][iw].y);
-      }
-    }
+    for (int j = 0; j < IGP_T; ++j) am[j] = sm.am[buf][bb][j];
+    sacc_band<NW, IGP_T, COUNT, FAST>(an, am, wx, wtr, wti2, qn, S1, S2, Sf, cnt);
   }
-  cp_async_wait<0>();
+}
+
+template <int NW, int IGP_T>
+constexpr size_t sacc_smem_bytes() {
+  return sizeof(SaccSmem<NW, IGP_T>);
 }
 
 template <int NW, int IGP_T, bool COUNT>
 __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_constant__ Params p,
                                                                const __grid_constant__ WxTable wxt) {
-  __shared__ __align__(16) double2 s_am[kSaccChunk][IGP_T];
-  __shared__ __align__(16) double2 s_an[kAnDepth][kThreads];
-  __shared__ double s_acc[4 * NW][kThreads];  // this thread's ach/asx partials
+  extern __shared__ __align__(16) unsigned char sacc_smem_raw[];
+  SaccSmem<NW, IGP_T>& sm = *reinterpret_cast<SaccSmem<NW, IGP_T>*>(sacc_smem_raw);
   const int tid = threadIdx.x;
 #pragma unroll
-  for (int k = 0; k < 4 * NW; ++k) s_acc[k][tid] = 0.0;
+  for (int k = 0; k < 4 * NW; ++k) sm.acc[k][tid] = 0.0;
   Acc<1> cnt;
   cnt.nn = 0;
   cnt.nf = 0;
 
   // n_items < 2^31 (host-checked): items decompose by multiply-shift.
-  for (unsigned item = blockIdx.x; item < static_cast<unsigned>(p.n_items); item += gridDim.x) {
-    const unsigned rest = fastdiv(item, p.igpt_mul, p.igpt_shift);
-    const int igpt = static_cast<int>(item - rest * p.n_igptile);
-    const unsigned bcu = fastdiv(rest, p.igblk_mul, p.igblk_shift);
-    const int igb = static_cast<int>(rest - bcu * p.n_igblk);
-    const int bc = static_cast<int>(bcu);
-    const int ig = (p.igblk0 + igb) * kThreads + tid;
-    const bool vig = ig < p.ncouls;
-    const int igc = vig ? ig : p.ncouls - 1;
-    const int b0 = bc * p.bchunk;
-    const int nb = min(p.bchunk, p.nbands - b0);
+  const unsigned n_items = static_cast<unsigned>(p.n_items);
+  unsigned item = blockIdx.x;
+  const double2* anp;
+  {
+    const SaccItem it0 = sacc_item(p, item);
+    anp = p.aqsn + static_cast<size_t>(p.band0 + it0.b0) * p.ncouls + sacc_igc(p, it0);
+    // First item: stage buffer 0 (its own group).
+    if (item < n_items) sacc_stage(p, it0, sm, 0);
+  }
+  cp_async_commit();
+  int buf = 0;
+  unsigned ro = 0;
+  bool primed = false;  // this item's first bands are already in the ring
+  bool deep = true;     // its staging group is older than the last kAnDepth - 1 groups
 
-    const double2* anp = p.aqsn + static_cast<size_t>(p.band0 + b0) * p.ncouls + igc;
-
-    // Item prologue: the aqsmtemp tile (-> shared), the first aqsntemp ring
-    // bands and wtilde are independent loads, so all three are in flight at
-    // once instead of three exposed latencies in a row.  The barrier first
-    // retires the previous item's reads of s_am.
-    __syncthreads();
-    for (int k = tid; k < nb * IGP_T; k += kThreads) {
-      const int bb = k / IGP_T, j = k - bb * IGP_T;
-      const int igp = igpt * IGP_T + j;
-      if (igp < p.ngpown)
-        cp_async16(&s_am[bb][j], p.aqsm + static_cast<size_t>(p.band0 + b0 + bb) * p.ngpown + igp);
-      else
-        s_am[bb][j] = make_double2(0.0, 0.0);
+  while (item < n_items) {
+    // Decomposed afresh from the uniform item index every iteration (not
+    // carried), so the band offset stays on the uniform datapath.
+    const SaccItem it = sacc_item(p, item);
+    if (!primed) {
+      // Prime the ring (first item, or after an item too short to do it).
+      cp_async_wait<0>();
+      ro = 0;
+#pragma unroll
+      for (int s = 0; s < kAnDepth - 1; ++s) {
+        if (s < it.nb) cp_async16(&sm.an[s][tid], anp + static_cast<size_t>(s) * p.ncouls);
+        cp_async_commit();
+      }
+      deep = true;
     }
-    cp_async_commit();
-    sacc_prefill(anp, p.ncouls, nb, s_an);
+    const unsigned nitem = item + gridDim.x;
+    const bool has_next = nitem < n_items;
+    const SaccItem nx = sacc_item(p, has_next ? nitem : item);
+    const double2* nx_anp =
+        p.aqsn + static_cast<size_t>(p.band0 + nx.b0) * p.ncouls + sacc_igc(p, nx);
+    const int ig = (p.igblk0 + it.igb) * kThreads + tid;
+    const bool vig = ig < p.ncouls;
 
+    // This item's staging has landed (per thread); the barrier publishes the
+    // aqsmtemp tile and retires the previous item's reads of the other buffer.
+    if (deep)
+      cp_async_wait<kAnDepth - 1>();
+    else
+      cp_async_wait<0>();
     double wtr[IGP_T], wti2[IGP_T], qn[IGP_T];
     bool thread_regular = true;
 #pragma unroll
     for (int j = 0; j < IGP_T; ++j) {
-      const int igp = igpt * IGP_T + j;
+      const int igp = it.igpt * IGP_T + j;
       const bool v = vig && igp < p.ngpown;
-      const size_t off = static_cast<size_t>(min(igp, p.ngpown - 1)) * p.ncouls + igc;
-      const double2 wt = __ldg(p.wtilde + off);
+      const double2 wt = sm.we[buf][j][0][tid];
       wtr[j] = wt.x;
       wti2[j] = wt.y * wt.y;
       const double wt2 = fma(wt.x, wt.x, wti2[j]);
@@ -854,7 +948,6 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
       const double m = p.wxmax + sqrt(wt2);
       thread_regular = thread_regular && (!v || (wt.y != 0.0 && wt2 > 1.000001e-24 * m * m));
     }
-    cp_async_wait<kAnDepth - 1>();  // this thread's s_am copies (the ring may still fly)
     const bool item_regular = __syncthreads_and(!COUNT && thread_regular) != 0;
 
     double2 S1[IGP_T][NW], S2[IGP_T][NW], Sf[IGP_T][NW];
@@ -867,23 +960,23 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
         Sf[j][iw] = make_double2(0.0, 0.0);
       }
     if (item_regular)
-      sacc_band_loop<NW, IGP_T, COUNT, true>(anp, p.ncouls, nb, s_an, s_am, wxt, b0 * NW, wtr,
-                                             wti2, qn, S1, S2, Sf, cnt);
+      sacc_band_loop<NW, IGP_T, COUNT, true>(p, wxt, sm, buf, ro, it, anp, has_next, nx, nx_anp,
+                                             wtr, wti2, qn, S1, S2, Sf, cnt);
     else
-      sacc_band_loop<NW, IGP_T, COUNT, false>(anp, p.ncouls, nb, s_an, s_am, wxt, b0 * NW, wtr,
-                                              wti2, qn, S1, S2, Sf, cnt);
+      sacc_band_loop<NW, IGP_T, COUNT, false>(p, wxt, sm, buf, ro, it, anp, has_next, nx, nx_anp,
+                                              wtr, wti2, qn, S1, S2, Sf, cnt);
 
-    // Item epilogue: apply the (ig, igp) constants once.
+    // Item epilogue: apply the (ig, igp) constants once (wtilde / eps from
+    // the staged buffer: no load latency here).
     double a[4 * NW];
 #pragma unroll
-    for (int k = 0; k < 4 * NW; ++k) a[k] = s_acc[k][tid];
+    for (int k = 0; k < 4 * NW; ++k) a[k] = sm.acc[k][tid];
 #pragma unroll
     for (int j = 0; j < IGP_T; ++j) {
-      const int igp = igpt * IGP_T + j;
+      const int igp = it.igpt * IGP_T + j;
       const bool v = vig && igp < p.ngpown;
-      const size_t off = static_cast<size_t>(min(igp, p.ngpown - 1)) * p.ncouls + igc;
-      const double2 wt = __ldg(p.wtilde + off);
-      const double2 e = v ? __ldg(p.eps + off) : make_double2(0.0, 0.0);
+      const double2 wt = sm.we[buf][j][0][tid];
+      const double2 e = v ? sm.we[buf][j][1][tid] : make_double2(0.0, 0.0);
       const double wt2 = fma(wt.x, wt.x, wt.y * wt.y);
       const double c1r = e.x * wt.x - e.y * wt.y, c1i = e.x * wt.y + e.y * wt.x;  // eps wt
       const double c2r = e.x * wt2, c2i = e.y * wt2;                              // eps |wt|^2
@@ -899,25 +992,35 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
       }
     }
 #pragma unroll
-    for (int k = 0; k < 4 * NW; ++k) s_acc[k][tid] = a[k];
-  }
+    for (int k = 0; k < 4 * NW; ++k) sm.acc[k][tid] = a[k];
 
-  // CTA reduction straight from s_acc (no extra shared scratch, so a 256-band
-  // chunk fits the 48 KB static limit): warp w sums rows w, w + 8, ... in a
+    if (!has_next) break;
+    // The staging group (iteration 0) is older than the last kAnDepth - 1
+    // groups only if the item ran at least kAnDepth bands.
+    deep = it.nb >= kAnDepth;
+    primed = it.nb >= kAnDepth - 1;
+    ro = (ro + static_cast<unsigned>(it.nb)) % kAnDepth;
+    buf ^= 1;
+    item = nitem;
+    anp = nx_anp;
+  }
+  cp_async_wait<0>();
+
+  // CTA reduction straight from sm.acc: warp w sums rows w, w + 8, ... in a
   // fixed order -- eight strided elements per lane, then an xor tree.
   __syncthreads();
   const int lane = tid & 31, warp = tid >> 5;
   for (int k = warp; k < 4 * NW; k += kThreads / 32) {
     double v = 0.0;
 #pragma unroll
-    for (int i = 0; i < kThreads / 32; ++i) v += s_acc[k][lane + 32 * i];
+    for (int i = 0; i < kThreads / 32; ++i) v += sm.acc[k][lane + 32 * i];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
     if (lane == 0) p.partials[static_cast<size_t>(blockIdx.x) * (4 * NW) + k] = v;
   }
   if constexpr (COUNT) {
     // The aqsntemp ring is idle now: reuse it for the per-warp counts.
-    unsigned long long* s_cnt = reinterpret_cast<unsigned long long*>(&s_an[0][0]);
+    unsigned long long* s_cnt = reinterpret_cast<unsigned long long*>(&sm.an[0][0]);
     unsigned long long cn = cnt.nn, cf = cnt.nf;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {

@@ -165,6 +165,7 @@ using SaccFn = void (*)(gpp::Params, gpp::WxTable);
 struct KernelRef {
   KernelFn fn = nullptr;
   SaccFn sacc = nullptr;
+  size_t smem = 0;  // dynamic shared memory of the sacc kernels
   const void* ptr() const {
     return fn ? reinterpret_cast<const void*>(fn) : reinterpret_cast<const void*>(sacc);
   }
@@ -227,18 +228,28 @@ KernelFn pick_plain(int nw) {
 // whose S sums fit the 128-register budget without spills (ptxas -v).
 // Four-frequency groups keep the one-seed kernel (FastPolicy3): their S sums
 // do not fit beside the ach/asx shared-memory slab.
-int sacc_igp(int nw) { return nw <= 1 ? 4 : (nw == 2 ? 3 : (nw == 3 ? 2 : 3)); }
+int sacc_igp(int nw) { return nw <= 1 ? 3 : (nw == 2 ? 3 : (nw == 3 ? 2 : 3)); }
+
+template <int NW, int IGP_T, bool C>
+KernelRef sacc_ref() {
+  KernelRef k;
+  k.sacc = gpp::gpp_sacc_kernel<NW, IGP_T, C>;
+  k.smem = gpp::sacc_smem_bytes<NW, IGP_T>();
+  return k;
+}
 
 template <bool C>
 KernelRef pick_sacc(int nw) {
-  KernelRef k;
   switch (nw) {
-    case 1: k.sacc = gpp::gpp_sacc_kernel<1, 4, C>; break;
-    case 2: k.sacc = gpp::gpp_sacc_kernel<2, 3, C>; break;
-    case 3: k.sacc = gpp::gpp_sacc_kernel<3, 2, C>; break;
-    default: k.fn = gpp::gpp_main_kernel<gpp::FastPolicy, 4, 3, C>; break;
+    case 1: return sacc_ref<1, 3, C>();
+    case 2: return sacc_ref<2, 3, C>();
+    case 3: return sacc_ref<3, 2, C>();
+    default: {
+      KernelRef k;
+      k.fn = gpp::gpp_main_kernel<gpp::FastPolicy, 4, 3, C>;
+      return k;
+    }
   }
-  return k;
 }
 
 template <bool C>
@@ -325,7 +336,12 @@ int make_plan_uncached(gpp_ctx* c, int variant, int nw_group, bool count, Plan* 
   pl->n_igptile = static_cast<int>((c->ngpown + pl->igp_t - 1) / pl->igp_t);
   const KernelRef fn = pick_kernel(variant, nw_group, pl->igp_t, count);
   int bps = 0;
-  GPP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn.ptr(), gpp::kThreads, 0));
+  // Dynamic shared memory above the 48 KB default needs an opt-in (per device:
+  // plans are made per context, with its device current).
+  if (fn.smem > 0)
+    GPP_CUDA(cudaFuncSetAttribute(fn.ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(fn.smem)));
+  GPP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn.ptr(), gpp::kThreads, fn.smem));
   cudaFuncAttributes attr;
   GPP_CUDA(cudaFuncGetAttributes(&attr, fn.ptr()));
   pl->regs = attr.numRegs;
@@ -461,7 +477,7 @@ int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool
           for (int64_t b = 0; b < wnb; ++b)
             for (int iw = 0; iw < nwg; ++iw)
               t.w[b * nwg + iw] = c->h_wx[(wb0 + b) * c->nw + iw0 + iw];
-          fn.sacc<<<grid, gpp::kThreads, 0, ks>>>(p, t);
+          fn.sacc<<<grid, gpp::kThreads, fn.smem, ks>>>(p, t);
         } else {
           fn.fn<<<grid, gpp::kThreads, 0, ks>>>(p);
         }

@@ -14,5 +14,6 @@
 #if defined(KERNEL) && KERNEL == 1
 template __global__ void gpp::gpp_main_kernel<POLICY, NWV, IGPV, false>(gpp::Params);
 #else
-template __global__ void gpp::gpp_sacc_kernel<NWV, IGPV, false>(const __grid_constant__ gpp::Params, const __grid_constant__ gpp::WxTable);
+template __global__ void gpp::gpp_sacc_kernel<NWV, IGPV, false>(const __grid_constant__ gpp::Params,
+                                                              const __grid_constant__ gpp::WxTable);
 #endif
