@@ -822,7 +822,6 @@ __device__ __forceinline__ void sacc_band_loop(const Params& p, const WxTable& w
                                                SaccSmem<NW, IGP_T>& sm, int buf, unsigned ro,
                                                const SaccItem& it, const double2* anp,
                                                bool has_next, const SaccItem& nx,
-                                               const double2* nx_anp,
                                                const double (&wtr)[IGP_T],
                                                const double (&wti2)[IGP_T],
                                                const double (&qn)[IGP_T],
@@ -837,7 +836,32 @@ __device__ __forceinline__ void sacc_band_loop(const Params& p, const WxTable& w
   // The next item's staging joins iteration 0's commit group.
   if (has_next) sacc_stage(p, nx, sm, buf ^ 1);
   int wxo = wx0;
-  for (int bb = 0; bb < nmain; ++bb) {
+  // Main phase unrolled by the ring depth: the four ring slots of a round
+  // are fixed per item, so no slot arithmetic in the loop.
+  const int nmain4 = nmain & ~(kAnDepth - 1);
+  double2* slot[kAnDepth];
+#pragma unroll
+  for (int k = 0; k < kAnDepth; ++k) slot[k] = &sm.an[(ro + k) % kAnDepth][tid];
+  for (int b4 = 0; b4 < nmain4; b4 += kAnDepth) {
+#pragma unroll
+    for (int k = 0; k < kAnDepth; ++k) {
+      const int bb = b4 + k;
+      cp_async16(slot[(k + kAnDepth - 1) % kAnDepth], pfp);
+      pfp += ncouls;
+      cp_async_commit();
+      cp_async_wait<kAnDepth - 1>();
+      const double2 an = *slot[k];
+      double wx[NW];
+#pragma unroll
+      for (int iw = 0; iw < NW; ++iw) wx[iw] = wxt.w[wxo + iw];
+      wxo += NW;
+      double2 am[IGP_T];
+#pragma unroll
+      for (int j = 0; j < IGP_T; ++j) am[j] = sm.am[buf][bb][j];
+      sacc_band<NW, IGP_T, COUNT, FAST>(an, am, wx, wtr, wti2, qn, S1, S2, Sf, cnt);
+    }
+  }
+  for (int bb = nmain4; bb < nmain; ++bb) {
     cp_async16(&sm.an[(ro + bb + kAnDepth - 1) % kAnDepth][tid], pfp);  // unsigned: a mask
     pfp += ncouls;
     cp_async_commit();
@@ -852,12 +876,17 @@ __device__ __forceinline__ void sacc_band_loop(const Params& p, const WxTable& w
     for (int j = 0; j < IGP_T; ++j) am[j] = sm.am[buf][bb][j];
     sacc_band<NW, IGP_T, COUNT, FAST>(an, am, wx, wtr, wti2, qn, S1, S2, Sf, cnt);
   }
+  // The next item's column pointer is formed only here, so it is not live
+  // (two registers) across the main phase.
+  const double2* nx_anp =
+      p.aqsn + static_cast<size_t>(p.band0 + nx.b0) * p.ncouls + sacc_igc(p, nx);
   for (int bb = nmain; bb < nb; ++bb) {
     const int pf = bb + kAnDepth - 1;
     if (pf < nb)
-      cp_async16(&sm.an[(ro + pf) % kAnDepth][tid], anp + static_cast<size_t>(pf) * ncouls);
+      cp_async16(&sm.an[(ro + pf) % kAnDepth][tid], pfp);
     else if (has_next && nb >= kAnDepth - 1 && pf - nb < nx.nb)
       cp_async16(&sm.an[(ro + pf) % kAnDepth][tid], nx_anp + static_cast<size_t>(pf - nb) * ncouls);
+    pfp += ncouls;
     cp_async_commit();
     cp_async_wait<kAnDepth - 1>();
     const double2 an = sm.an[(ro + bb) % kAnDepth][tid];
@@ -891,13 +920,8 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
   // n_items < 2^31 (host-checked): items decompose by multiply-shift.
   const unsigned n_items = static_cast<unsigned>(p.n_items);
   unsigned item = blockIdx.x;
-  const double2* anp;
-  {
-    const SaccItem it0 = sacc_item(p, item);
-    anp = p.aqsn + static_cast<size_t>(p.band0 + it0.b0) * p.ncouls + sacc_igc(p, it0);
-    // First item: stage buffer 0 (its own group).
-    if (item < n_items) sacc_stage(p, it0, sm, 0);
-  }
+  // First item: stage buffer 0 (its own group).
+  if (item < n_items) sacc_stage(p, sacc_item(p, item), sm, 0);
   cp_async_commit();
   int buf = 0;
   unsigned ro = 0;
@@ -908,6 +932,8 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
     // Decomposed afresh from the uniform item index every iteration (not
     // carried), so the band offset stays on the uniform datapath.
     const SaccItem it = sacc_item(p, item);
+    const double2* anp =
+        p.aqsn + static_cast<size_t>(p.band0 + it.b0) * p.ncouls + sacc_igc(p, it);
     if (!primed) {
       // Prime the ring (first item, or after an item too short to do it).
       cp_async_wait<0>();
@@ -922,8 +948,6 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
     const unsigned nitem = item + gridDim.x;
     const bool has_next = nitem < n_items;
     const SaccItem nx = sacc_item(p, has_next ? nitem : item);
-    const double2* nx_anp =
-        p.aqsn + static_cast<size_t>(p.band0 + nx.b0) * p.ncouls + sacc_igc(p, nx);
     const int ig = (p.igblk0 + it.igb) * kThreads + tid;
     const bool vig = ig < p.ncouls;
 
@@ -960,11 +984,11 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
         Sf[j][iw] = make_double2(0.0, 0.0);
       }
     if (item_regular)
-      sacc_band_loop<NW, IGP_T, COUNT, true>(p, wxt, sm, buf, ro, it, anp, has_next, nx, nx_anp,
-                                             wtr, wti2, qn, S1, S2, Sf, cnt);
+      sacc_band_loop<NW, IGP_T, COUNT, true>(p, wxt, sm, buf, ro, it, anp, has_next, nx, wtr,
+                                             wti2, qn, S1, S2, Sf, cnt);
     else
-      sacc_band_loop<NW, IGP_T, COUNT, false>(p, wxt, sm, buf, ro, it, anp, has_next, nx, nx_anp,
-                                              wtr, wti2, qn, S1, S2, Sf, cnt);
+      sacc_band_loop<NW, IGP_T, COUNT, false>(p, wxt, sm, buf, ro, it, anp, has_next, nx, wtr,
+                                              wti2, qn, S1, S2, Sf, cnt);
 
     // Item epilogue: apply the (ig, igp) constants once (wtilde / eps from
     // the staged buffer: no load latency here).
@@ -1002,7 +1026,6 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
     ro = (ro + static_cast<unsigned>(it.nb)) % kAnDepth;
     buf ^= 1;
     item = nitem;
-    anp = nx_anp;
   }
   cp_async_wait<0>();
 
