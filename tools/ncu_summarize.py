@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--json")
     ap.add_argument("--algorithmic-flops", type=float)
     ap.add_argument("--note", default="")
+    ap.add_argument("--workload", default="512,66,32768,3,1",
+                    help="nbands,ngpown,ncouls,nw,seed of the capture (tools/profile_run.py defaults)")
     a = ap.parse_args()
 
     raw = list(csv.reader(io.StringIO(ncu(a.report, "--page", "raw", "--csv"))))
@@ -113,6 +115,8 @@ def main():
             "fp64_pipe_pct": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
             "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
         }
+        nb, ng, nc, nw, seed = (int(x) for x in a.workload.split(","))
+        summary["workload"] = {"dims": [nb, ng, nc], "nw": nw, "seed": seed, "variant": "rcp_sq"}
         Path(a.json).write_text(json.dumps(summary, indent=1) + "\n")
 
 
