@@ -60,6 +60,14 @@ struct Params {
   // band offset indexing the WxTable stays in a uniform register.
   unsigned long long igpt_mul, igblk_mul;
   int igpt_shift, igblk_shift;
+  // gpp_sacc_kernel enumerates rows [row0, row0 + n_rows) of (igb, igp tile)
+  // pairs (tile fastest; row = igb * n_igptile + tile) times band chunks of
+  // its window: item = chunk * n_rows + (row - row0).  A whole launch has
+  // row0 = 0 and n_rows = n_igblk * n_igptile; a balanced-tail launch covers
+  // the last rows of the last chunk in finer chunks (host: enqueue_eval).
+  int row0, n_rows;
+  unsigned long long rows_mul;
+  int rows_shift;
   double wxmax;            // max |wx| over the uploaded bands (regular-item guard)
   double* partials;                 // [gridDim.x][4 * NW]
   unsigned long long* cpartials;    // [gridDim.x][2]
@@ -681,10 +689,11 @@ struct SaccItem {
 
 __device__ __forceinline__ SaccItem sacc_item(const Params& p, unsigned item) {
   SaccItem it;
-  const unsigned rest = fastdiv(item, p.igpt_mul, p.igpt_shift);
-  it.igpt = static_cast<int>(item - rest * p.n_igptile);
-  const unsigned bcu = fastdiv(rest, p.igblk_mul, p.igblk_shift);
-  it.igb = static_cast<int>(rest - bcu * p.n_igblk);
+  const unsigned bcu = fastdiv(item, p.rows_mul, p.rows_shift);
+  const unsigned row = item - bcu * static_cast<unsigned>(p.n_rows) + static_cast<unsigned>(p.row0);
+  const unsigned igb = fastdiv(row, p.igpt_mul, p.igpt_shift);
+  it.igpt = static_cast<int>(row - igb * p.n_igptile);
+  it.igb = static_cast<int>(igb);
   it.b0 = static_cast<int>(bcu) * p.bchunk;
   it.nb = min(p.bchunk, p.nbands - it.b0);
   return it;

@@ -390,6 +390,46 @@ int nw_groups(int nw, std::vector<std::pair<int, int>>* groups) {
   return GPP_OK;
 }
 
+// One launch of the production kernel: rows [row0, row0 + n_rows) of (igb,
+// igp tile) pairs times the band chunks of the window [wb0, wb0 + wnb).
+struct SaccLaunch {
+  int row0, n_rows;
+  int64_t wb0, wnb;
+  int bchunk;
+  long long n_items;
+};
+
+// Balanced tail: the static round-robin leaves the last wave's R items (the
+// last R rows of the last band chunk) on R of the `slots` resident CTAs while
+// the others idle.  If that wave is partial, run the whole waves as one launch
+// and those R rows' last chunk as a second launch cut into finer band chunks,
+// when the modelled makespan (waves x (chunk + per-item overhead)) drops.
+void split_tail(std::vector<SaccLaunch>& ls, long long slots) {
+  constexpr double kItemOverheadBands = 4.0;
+  const SaccLaunch L = ls[0];
+  const long long R = L.n_items % slots, full = L.n_items / slots;
+  if (full < 1 || R == 0 || R > L.n_rows) return;
+  const int64_t n_chunks = (L.wnb + L.bchunk - 1) / L.bchunk;
+  const int64_t last_b0 = (n_chunks - 1) * L.bchunk, nb_last = L.wnb - last_b0;
+  const double base = static_cast<double>(nb_last) + kItemOverheadBands;
+  double best = base;
+  int best_bc = 0;
+  for (int64_t k = 2; k <= nb_last; ++k) {
+    const int64_t bc = (nb_last + k - 1) / k, subs = (nb_last + bc - 1) / bc;
+    const long long waves = (R * subs + slots - 1) / slots;
+    const double cost = static_cast<double>(waves) * (static_cast<double>(bc) + kItemOverheadBands);
+    if (cost < best - 0.5) {
+      best = cost;
+      best_bc = static_cast<int>(bc);
+    }
+  }
+  if (best_bc == 0) return;
+  ls[0].n_items = full * slots;
+  const int64_t subs = (nb_last + best_bc - 1) / best_bc;
+  ls.push_back({L.n_rows - static_cast<int>(R), static_cast<int>(R), L.wb0 + last_b0, nb_last,
+                best_bc, R * subs});
+}
+
 // Optional ig-slab schedule of one evaluation: slab s covers the 256-ig blocks
 // [blk0[s], blk0[s+1]) and its launch waits on ready[s] (the H2D of its rows).
 struct SlabSched {
@@ -422,15 +462,18 @@ int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool
     const int n_win = static_cast<int>((c->nbands + win - 1) / win);
     if (fn.sacc && pl.n_items >= (1ll << 31))
       return fail(GPP_ERR_ARG, "too many work items for one launch");
-    GPP_CUDA(c->partials.ensure(static_cast<size_t>(pl.grid) * n_slabs * n_win * 4 *
+    // Up to two launches (whole waves + balanced tail) per slab and window.
+    GPP_CUDA(c->partials.ensure(static_cast<size_t>(pl.grid) * n_slabs * n_win * 2 * 4 *
                                 gpp::kMaxNwGroup));
-    GPP_CUDA(c->cpartials.ensure(static_cast<size_t>(pl.grid) * n_slabs * n_win * 2));
+    GPP_CUDA(c->cpartials.ensure(static_cast<size_t>(pl.grid) * n_slabs * n_win * 2 * 2));
     int rows = 0;  // partial rows written by this frequency group
     if (ev_main && gi == 0) GPP_CUDA(cudaEventRecord(ev_main[0], c->stream));
     // Slabs alternate between two streams so that slab s+1's CTAs fill the
     // SMs that slab s's last wave leaves idle (each slab writes its own
     // partial rows; the finalize joins both streams).
-    const bool two = n_slabs > 1;
+    // (The production kernel also runs its balanced tail launches on the
+    // other stream, where they fill the SMs its whole waves free up.)
+    const bool two = n_slabs > 1 || fn.sacc;
     if (two) {
       GPP_CUDA(cudaEventRecord(c->ev_fork, c->stream));
       GPP_CUDA(cudaStreamWaitEvent(c->kstream2, c->ev_fork, 0));
@@ -442,47 +485,64 @@ int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool
       if (gi == 0 && !sl.ready.empty()) GPP_CUDA(cudaStreamWaitEvent(ks, sl.ready[s], 0));
       for (int w = 0; w < n_win; ++w) {
         const int64_t wb0 = w * win, wnb = std::min<int64_t>(win, c->nbands - wb0);
-        gpp::Params p;
-        p.wtilde = c->wtilde.ptr;
-        p.eps = c->eps.ptr;
-        p.aqsn = c->aqsn.ptr;
-        p.aqsm = c->aqsm.ptr;
-        p.wxb = c->wxb.ptr;
-        p.ncouls = static_cast<int>(c->ncouls);
-        p.ngpown = static_cast<int>(c->ngpown);
-        p.nbands = static_cast<int>(wnb);
-        p.band0 = static_cast<int>(wb0);
-        p.nw_total = c->nw;
-        p.iw0 = iw0;
-        p.igblk0 = sl.blk0[s];
-        p.n_igblk = nblk;
-        p.n_igptile = pl.n_igptile;
-        gpp::fastdiv_init(static_cast<unsigned>(p.n_igptile), &p.igpt_mul, &p.igpt_shift);
-        gpp::fastdiv_init(static_cast<unsigned>(p.n_igblk), &p.igblk_mul, &p.igblk_shift);
+        const long long slots = static_cast<long long>(pl.blocks_per_sm) * c->num_sms;
         // A slab (or band window) re-plans its band chunk for its own item
         // count: short chunks keep the last (small) slabs from idling most of
         // the SMs.
-        p.bchunk = (nblk == pl.n_igblk && wnb == c->nbands)
-                       ? pl.bchunk
-                       : choose_bchunk(nblk, pl.n_igptile, wnb,
-                                       static_cast<long long>(pl.blocks_per_sm) * c->num_sms,
-                                       fn.sacc ? gpp::kSaccChunk : gpp::kMaxChunk);
-        p.n_items = static_cast<long long>(nblk) * pl.n_igptile * ((wnb + p.bchunk - 1) / p.bchunk);
-        p.wxmax = c->wxmax;
-        const int grid = static_cast<int>(std::min<long long>(pl.grid, p.n_items));
-        p.partials = c->partials.ptr + static_cast<size_t>(rows) * 4 * nwg;
-        p.cpartials = c->cpartials.ptr + static_cast<size_t>(rows) * 2;
-        if (fn.sacc) {
-          gpp::WxTable t;
-          for (int64_t b = 0; b < wnb; ++b)
-            for (int iw = 0; iw < nwg; ++iw)
-              t.w[b * nwg + iw] = c->h_wx[(wb0 + b) * c->nw + iw0 + iw];
-          fn.sacc<<<grid, gpp::kThreads, fn.smem, ks>>>(p, t);
-        } else {
-          fn.fn<<<grid, gpp::kThreads, 0, ks>>>(p);
+        const int bchunk = (nblk == pl.n_igblk && wnb == c->nbands)
+                               ? pl.bchunk
+                               : choose_bchunk(nblk, pl.n_igptile, wnb, slots,
+                                               fn.sacc ? gpp::kSaccChunk : gpp::kMaxChunk);
+        const int n_rows = nblk * pl.n_igptile;
+        const long long n_chunks = (wnb + bchunk - 1) / bchunk;
+        std::vector<SaccLaunch> launches{{0, n_rows, wb0, wnb, bchunk,
+                                          static_cast<long long>(n_rows) * n_chunks}};
+        if (fn.sacc) split_tail(launches, slots);
+        for (size_t li = 0; li < launches.size(); ++li) {
+          const SaccLaunch& L = launches[li];
+          cudaStream_t ls = ks;
+          if (li > 0) {  // balanced tail: independent items, on the other stream
+            ls = ks == c->stream ? c->kstream2 : c->stream;
+            if (gi == 0 && !sl.ready.empty()) GPP_CUDA(cudaStreamWaitEvent(ls, sl.ready[s], 0));
+          }
+          gpp::Params p;
+          p.wtilde = c->wtilde.ptr;
+          p.eps = c->eps.ptr;
+          p.aqsn = c->aqsn.ptr;
+          p.aqsm = c->aqsm.ptr;
+          p.wxb = c->wxb.ptr;
+          p.ncouls = static_cast<int>(c->ncouls);
+          p.ngpown = static_cast<int>(c->ngpown);
+          p.nbands = static_cast<int>(L.wnb);
+          p.band0 = static_cast<int>(L.wb0);
+          p.nw_total = c->nw;
+          p.iw0 = iw0;
+          p.igblk0 = sl.blk0[s];
+          p.n_igblk = nblk;
+          p.n_igptile = pl.n_igptile;
+          p.row0 = L.row0;
+          p.n_rows = L.n_rows;
+          gpp::fastdiv_init(static_cast<unsigned>(p.n_igptile), &p.igpt_mul, &p.igpt_shift);
+          gpp::fastdiv_init(static_cast<unsigned>(p.n_igblk), &p.igblk_mul, &p.igblk_shift);
+          gpp::fastdiv_init(static_cast<unsigned>(p.n_rows), &p.rows_mul, &p.rows_shift);
+          p.bchunk = L.bchunk;
+          p.n_items = L.n_items;
+          p.wxmax = c->wxmax;
+          const int grid = static_cast<int>(std::min<long long>(pl.grid, p.n_items));
+          p.partials = c->partials.ptr + static_cast<size_t>(rows) * 4 * nwg;
+          p.cpartials = c->cpartials.ptr + static_cast<size_t>(rows) * 2;
+          if (fn.sacc) {
+            gpp::WxTable t;
+            for (int64_t b = 0; b < L.wnb; ++b)
+              for (int iw = 0; iw < nwg; ++iw)
+                t.w[b * nwg + iw] = c->h_wx[(L.wb0 + b) * c->nw + iw0 + iw];
+            fn.sacc<<<grid, gpp::kThreads, fn.smem, ls>>>(p, t);
+          } else {
+            fn.fn<<<grid, gpp::kThreads, 0, ls>>>(p);
+          }
+          GPP_CUDA(cudaGetLastError());
+          rows += grid;
         }
-        GPP_CUDA(cudaGetLastError());
-        rows += grid;
       }
     }
     if (two) {
