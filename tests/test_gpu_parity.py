@@ -378,3 +378,26 @@ def test_variant_terms_vs_oracle(variant):
         scale = max(np.abs(sch).max(), np.abs(ssx).max())
         assert np.abs(got.sch - sch).max() <= 1e-14 * scale
         assert np.abs(got.ssx - ssx).max() <= 1e-14 * scale
+
+
+# Schedules of the production kernel (csrc/gpp_lib.cu enqueue_eval): several
+# band windows of the by-value wx table (512 bands at nw 3, 768 at nw 2, 1536
+# at nw 1), the balanced-tail second launch, and items shorter than the
+# aqsntemp ring (the ring re-primes).  Oracle on the same inputs.
+@pytest.mark.parametrize("dims,nw", [
+    ((600, 3, 300), 3),      # two band windows, few items
+    ((1100, 2, 256), 2),     # two windows at nw 2
+    ((1600, 2, 300), 1),     # two windows at nw 1
+    ((258, 33, 8192), 3),    # 2-band last chunk (short items) + balanced tail
+    ((5, 7, 70000), 3),      # 5-band items, balanced tail of 5-band rows
+    ((2, 5, 40000), 1),      # every item shorter than the ring
+    ((1, 1, 1), 3),
+])
+def test_production_schedules_vs_oracle(dims, nw):
+    p = synth_problem(*dims, seed=5, nw=nw, check=False)
+    want = orc.evaluate_variant(p, "rcp_sq")
+    inst, near, far = orc.branch_stats(p, "rcp_sq")
+    got, stats, _ = evaluate(p, "rcp_sq")
+    assert max_rel_error(got, want) <= TOL
+    assert max_rel_error(evaluate_variant(p, "rcp_sq"), want) <= TOL
+    assert (stats.instances, stats.near, stats.far) == (inst, near, far)
