@@ -172,6 +172,11 @@ int gpp_kernel_info(gpp_ctx* ctx, int32_t variant, int32_t* registers_per_thread
                     int32_t* threads_per_block, int32_t* blocks_per_sm, int32_t* grid,
                     int32_t* igp_tile, int32_t* band_chunk);
 
+/* Number of kernels this context has launched so far (every compute,
+ * finalize, synthesis and factored-path launch): the bench's gpu_launches is
+ * the difference across its timed region. */
+int gpp_launch_count(gpp_ctx* ctx, int64_t* launches);
+
 /* NCCL plumbing for band sharding across ranks (one process per GPU).
  * The unique id (128 bytes) is created on rank 0 and broadcast by the host
  * (torch.distributed in the Python driver). */

@@ -85,6 +85,7 @@ struct DevBuf {
 
 struct gpp_ctx {
   int device = -1;
+  uint64_t launches = 0;  // kernels this context has launched (gpp_launch_count)
   bool initialized = false;
   cudaStream_t stream = nullptr;
   cudaStream_t cstream = nullptr;  // H2D copies of the pipelined evaluate
@@ -404,8 +405,19 @@ struct SaccLaunch {
 // the others idle.  If that wave is partial, run the whole waves as one launch
 // and those R rows' last chunk as a second launch cut into finer band chunks,
 // when the modelled makespan (waves x (chunk + per-item overhead)) drops.
+// GPP_BALANCED_TAIL=0 keeps one launch per slab and window: ncu captures of a
+// whole evaluation in one launch (tools/profile_run.py, tools/ladder.py).
+bool balanced_tail_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GPP_BALANCED_TAIL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void split_tail(std::vector<SaccLaunch>& ls, long long slots) {
   constexpr double kItemOverheadBands = 4.0;
+  if (!balanced_tail_enabled()) return;
   const SaccLaunch L = ls[0];
   const long long R = L.n_items % slots, full = L.n_items / slots;
   if (full < 1 || R == 0 || R > L.n_rows) return;
@@ -537,8 +549,10 @@ int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool
               for (int iw = 0; iw < nwg; ++iw)
                 t.w[b * nwg + iw] = c->h_wx[(L.wb0 + b) * c->nw + iw0 + iw];
             fn.sacc<<<grid, gpp::kThreads, fn.smem, ls>>>(p, t);
+            ++c->launches;
           } else {
             fn.fn<<<grid, gpp::kThreads, 0, ls>>>(p);
+            ++c->launches;
           }
           GPP_CUDA(cudaGetLastError());
           rows += grid;
@@ -550,6 +564,7 @@ int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool
       GPP_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     }
     if (ev_main && gi + 1 == groups.size()) GPP_CUDA(cudaEventRecord(ev_main[1], c->stream));
+    ++c->launches;
     pick_finalize(nwg)<<<1, 256, 0, c->stream>>>(c->partials.ptr, c->cpartials.ptr, rows,
                                                   c->nw, iw0, variant >= GPP_VARIANT_RCP_SQ,
                                                   first ? 1 : 0, count ? 1 : 0, c->out.ptr,
@@ -961,6 +976,12 @@ int gpp_time(gpp_ctx* c, int32_t variant, int32_t iters, float* total_ms, float*
   return result;
 }
 
+int gpp_launch_count(gpp_ctx* c, int64_t* launches) {
+  if (!c || !launches) return fail(GPP_ERR_ARG, "ctx / launches is NULL");
+  *launches = static_cast<int64_t>(c->launches);
+  return GPP_OK;
+}
+
 int gpp_kernel_info(gpp_ctx* c, int32_t variant, int32_t* registers_per_thread,
                     int32_t* threads_per_block, int32_t* blocks_per_sm, int32_t* grid,
                     int32_t* igp_tile, int32_t* band_chunk) {
@@ -1055,6 +1076,7 @@ int gpp_synth(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32_
   };
   for (const Block& b : blocks) {
     const int grid = static_cast<int>(std::min<long long>((b.rows + 255) / 256, 65535));
+    ++c->launches;
     gpp::gpp_synth_kernel<<<grid, 256, 0, c->stream>>>(st, inc, b.offset, b.rows, b.cols, b.c0,
                                                        b.c1, reinterpret_cast<double*>(b.dst),
                                                        b.comp);
@@ -1126,6 +1148,7 @@ int gpp_run_factored(gpp_ctx* c, int32_t variant, double* achtemp, double* asxte
 #undef GPP_FAC_NW
 #undef GPP_FAC
     GPP_CUDA(cudaGetLastError());
+    c->launches += 2;  // branch terms + finalize
     pick_finalize(nwg)<<<1, 256, 0, c->stream>>>(c->partials.ptr, c->cpartials.ptr, grid, c->nw,
                                                   iw0, 0, first ? 1 : 0, 1, c->out.ptr,
                                                   c->counts.ptr);
@@ -1171,6 +1194,7 @@ int gpp_variant_terms(gpp_ctx* c, int32_t variant, double* sch, double* ssx, uin
     else if (variant == GPP_VARIANT_RCP) GPP_VT(1);
     else GPP_VT(2);
 #undef GPP_VT
+    ++c->launches;
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(sch, d_sch.ptr, n * sizeof(double2), cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(ssx, d_ssx.ptr, n * sizeof(double2), cudaMemcpyDeviceToHost, c->stream);

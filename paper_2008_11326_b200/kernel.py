@@ -251,6 +251,12 @@ class GPPContext:
                                       ctypes.byref(tot), ctypes.byref(main)), "gpp_time")
         return float(tot.value), float(main.value)
 
+    def launch_count(self) -> int:
+        """Kernels this context has launched so far (gpp_launch_count)."""
+        n = ctypes.c_int64(0)
+        _lib.check(self._lib.gpp_launch_count(self._h, ctypes.byref(n)), "gpp_launch_count")
+        return int(n.value)
+
     def kernel_info(self, variant: str = "rcp_sq") -> dict:
         vals = [ctypes.c_int32() for _ in range(6)]
         _lib.check(self._lib.gpp_kernel_info(self._h, _variant_code(variant),

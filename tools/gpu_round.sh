@@ -15,5 +15,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   > gpurun_out/${tag}_ncu_bench.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on \
   --metrics smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum \
-  -k regex:gpp_sacc_kernel -s 1 -c 1 -o gpurun_out/${tag}_sacc -f python tools/profile_run.py > gpurun_out/${tag}_ncu_full.log 2>&1
+  -k regex:gpp_sacc_kernel -s 1 -c 1 -o gpurun_out/${tag}_sacc -f env GPP_BALANCED_TAIL=0 python tools/profile_run.py > gpurun_out/${tag}_ncu_full.log 2>&1
 tail -2 gpurun_out/${tag}_ncu_full.log

@@ -18,7 +18,8 @@ a = ap.parse_args()
 p = synth_problem(*a.dims, seed=a.seed, nw=a.nw, check=False)
 ctx = GPPContext(0)
 ctx.upload(p)
-# The production (uncounted) kernel, as evaluate_variant and bench.py run it:
+# The production (uncounted) kernel, as evaluate_variant and bench.py run it
+# (run with GPP_BALANCED_TAIL=0 so that one launch covers the whole problem):
 # profile with -k regex:gpp_sacc_kernel -s 1 -c 1 to capture the second launch.
 tot, main = ctx.time(a.variant, a.reps)
 print(a.variant, a.dims, "nw", a.nw, f"{main / a.reps:.3f} ms per launch")
