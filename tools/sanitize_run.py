@@ -1,5 +1,7 @@
 """Small evaluations for compute-sanitizer (memcheck / racecheck / synccheck):
-every kernel family, ragged shapes, both upload paths, nw groups > 4."""
+every kernel family, ragged shapes, both upload paths, nw groups > 4, and
+production-kernel schedules with several items per CTA (cross-item staging),
+a balanced tail launch and two band windows."""
 import sys
 
 sys.path.insert(0, ".")
@@ -13,4 +15,11 @@ for dims, nw in (((5, 3, 40), 2), ((47, 2, 33), 3), ((9, 7, 300), 5), ((16, 8, 5
         ctx.run(v, counts=True)
         ctx.run(v, counts=False)
     ctx.time("rcp_sq", 1)
+# Production schedules: (40, 5, 40000) = 471 items -> one whole wave of 296
+# CTAs plus a balanced tail; (600, 2, 40000) = two band windows at nw 3.
+for dims, nw in (((40, 5, 40000), 3), ((600, 2, 40000), 3), ((7, 3, 90000), 2)):
+    p = synth_problem(*dims, seed=1, nw=nw, check=False)
+    ctx.upload(p, force=True)
+    ctx.run("rcp_sq", counts=True)
+    ctx.run("rcp_sq", counts=False)
 print("sanitize run ok")
