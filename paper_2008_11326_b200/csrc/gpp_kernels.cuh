@@ -55,11 +55,12 @@ struct Params {
   int band0;               // first (local) band of this launch's band window (gpp_sacc_kernel)
   int n_igblk, n_igptile, bchunk;
   long long n_items;
-  // Division by n_igptile / n_igblk as multiply-shift (host: fastdiv_init), so
-  // that gpp_sacc_kernel decomposes its items on the uniform datapath and the
-  // band offset indexing the WxTable stays in a uniform register.
-  unsigned long long igpt_mul, igblk_mul;
-  int igpt_shift, igblk_shift;
+  // Division by n_igptile / n_rows (below) as multiply-shift (host:
+  // fastdiv_init), so that gpp_sacc_kernel decomposes its items on the
+  // uniform datapath and the band offset indexing the WxTable stays in a
+  // uniform register.
+  unsigned long long igpt_mul;
+  int igpt_shift;
   // gpp_sacc_kernel enumerates rows [row0, row0 + n_rows) of (igb, igp tile)
   // pairs (tile fastest; row = igb * n_igptile + tile) times band chunks of
   // its window: item = chunk * n_rows + (row - row0).  A whole launch has
@@ -116,17 +117,6 @@ __device__ __forceinline__ double rcp_refined(double d) {
   double e = fma(-d, r, 1.0);
   e = fma(e, e, e);
   return fma(e, r, r);
-}
-// sqrt(x) to ~1 ulp from an rsqrt seed: two coupled Newton steps.
-__device__ __forceinline__ double sqrt_refined(double x) {
-  double r = rsqrt_approx(x);
-  double g = x * r;          // ~ sqrt(x)
-  double h = 0.5 * r;        // ~ 1 / (2 sqrt(x))
-  double e = fma(-g, h, 0.5);
-  g = fma(g, e, g);
-  h = fma(h, e, h);
-  double res = fma(-g, g, x);
-  return fma(res, h, g);
 }
 
 // cp.async (LDGSTS) of one 16-byte aqsntemp element into this thread's slot

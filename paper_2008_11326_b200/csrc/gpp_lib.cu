@@ -535,7 +535,6 @@ int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool
           p.row0 = L.row0;
           p.n_rows = L.n_rows;
           gpp::fastdiv_init(static_cast<unsigned>(p.n_igptile), &p.igpt_mul, &p.igpt_shift);
-          gpp::fastdiv_init(static_cast<unsigned>(p.n_igblk), &p.igblk_mul, &p.igblk_shift);
           gpp::fastdiv_init(static_cast<unsigned>(p.n_rows), &p.rows_mul, &p.rows_shift);
           p.bchunk = L.bchunk;
           p.n_items = L.n_items;
