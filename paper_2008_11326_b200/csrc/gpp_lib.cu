@@ -384,10 +384,22 @@ int make_plan(gpp_ctx* c, int variant, int nw_group, bool count, Plan* pl) {
   return GPP_OK;
 }
 
-int nw_groups(int nw, std::vector<std::pair<int, int>>* groups) {
+// Frequency groups of one evaluation (one launch sequence each).  The
+// production kernel takes at most three frequencies per launch (its S sums
+// for four do not fit the register budget), so for nw >= 4 it runs
+// ceil(nw / 3) balanced groups -- e.g. 2 + 2 at nw 4 -- which the register-
+// file model rates at 46-49 reads per instance against 56 for the four-wide
+// one-seed kernel.  The other kernels take groups of four.
+int max_group(int variant) { return variant == GPP_VARIANT_RCP_SQ ? 3 : gpp::kMaxNwGroup; }
+
+int nw_groups(int nw, int gmax, std::vector<std::pair<int, int>>* groups) {
   groups->clear();
-  for (int iw0 = 0; iw0 < nw; iw0 += gpp::kMaxNwGroup)
-    groups->emplace_back(iw0, std::min(gpp::kMaxNwGroup, nw - iw0));
+  const int n = (nw + gmax - 1) / gmax;
+  for (int k = 0, iw0 = 0; k < n; ++k) {
+    const int sz = nw / n + (k < nw % n ? 1 : 0);
+    groups->emplace_back(iw0, sz);
+    iw0 += sz;
+  }
   return GPP_OK;
 }
 
@@ -454,7 +466,7 @@ struct SlabSched {
 int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool allreduce,
                  const SlabSched* sched = nullptr) {
   std::vector<std::pair<int, int>> groups;
-  nw_groups(c->nw, &groups);
+  nw_groups(c->nw, max_group(variant), &groups);
   const int n_blk_all = static_cast<int>((c->ncouls + gpp::kThreads - 1) / gpp::kThreads);
   SlabSched whole;
   whole.blk0 = {0, n_blk_all};
@@ -991,7 +1003,7 @@ int gpp_kernel_info(gpp_ctx* c, int32_t variant, int32_t* registers_per_thread,
   DeviceGuard g(c->device);
   if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
   Plan pl;
-  rc = make_plan(c, variant, std::min(c->nw, gpp::kMaxNwGroup), false, &pl);
+  rc = make_plan(c, variant, std::min(c->nw, max_group(variant)), false, &pl);
   if (rc) return rc;
   if (registers_per_thread) *registers_per_thread = pl.regs;
   if (threads_per_block) *threads_per_block = gpp::kThreads;
@@ -1117,7 +1129,7 @@ int gpp_run_factored(gpp_ctx* c, int32_t variant, double* achtemp, double* asxte
       static_cast<int>(c->ncouls));
   if (st != CUBLAS_STATUS_SUCCESS) return fail(GPP_ERR_CUDA, "cublasZgemm failed");
   std::vector<std::pair<int, int>> groups;
-  nw_groups(c->nw, &groups);
+  nw_groups(c->nw, gpp::kMaxNwGroup, &groups);
   const int grid = std::max(1, std::min<int>(c->num_sms * 4, static_cast<int>(
                                    (n_el + gpp::kThreads - 1) / gpp::kThreads)));
   GPP_CUDA(c->partials.ensure(static_cast<size_t>(grid) * 4 * gpp::kMaxNwGroup));
