@@ -52,12 +52,17 @@ def parse_args():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", choices=tuple(WORKLOADS), default="paper")
     ap.add_argument("--nw", type=int, default=3)
-    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--seed", type=int, default=None,
+                    help="synth_problem seed (default: 1; 42 for the weak workload, whose "
+                         "reference output tests/golden/gpp_big.json holds)")
     ap.add_argument("--variant", choices=("rcp_sq", "rcp", "div"), default="rcp_sq")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.seed is None:
+        a.seed = 42 if a.workload == "weak" else 1
+    return a
 
 
 # ----------------------------------------------------------------------------

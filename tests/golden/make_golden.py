@@ -15,6 +15,8 @@ nw=3 cases patch NW=3 into rooflab.gpp.problem, .kernel and .runner, the
 three modules that import it by value (SURVEY.md Table R).
 ``--big`` adds the paper size (512, 66, 32768) and the weak-scaled size
 (4096, 528, 65536); the weak case needs ~18 GB of RAM and ~1 minute.
+``--append weak-nw3`` adds the weak size at nw = 3 (the bench default) to an
+existing gpp_big.json.
 """
 
 from __future__ import annotations
@@ -98,7 +100,19 @@ def make_case(dims, seed, nw, with_reference: bool, versions: bool = True) -> di
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
+    ap.add_argument("--append", choices=("weak-nw3",),
+                    help="append one big case to the existing gpp_big.json and stop")
     args = ap.parse_args()
+
+    if args.append == "weak-nw3":
+        # The bench's weak workload at its default frequency count (nw 3).
+        path = HERE / "gpp_big.json"
+        big = json.loads(path.read_text())
+        big["cases"] = [c for c in big["cases"]
+                        if not (c["dims"] == [4096, 528, 65536] and c["seed"] == 42 and c["nw"] == 3)]
+        big["cases"].append(make_case((4096, 528, 65536), 42, 3, with_reference=False, versions=False))
+        path.write_text(json.dumps(big, indent=1) + "\n")
+        return
 
     cases = []
     for dims in SMALL_DIMS:
