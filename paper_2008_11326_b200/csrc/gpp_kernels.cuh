@@ -967,9 +967,11 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
       wti2[j] = wt.y * wt.y;
       const double wt2 = fma(wt.x, wt.x, wti2[j]);
       qn[j] = v ? fmax(0.25, 0.25 * wt2) : __longlong_as_double(0x7FF0000000000000ll);
-      // Regular (see FastPolicy3::regular): no instance can be degenerate.
-      const double m = p.wxmax + sqrt(wt2);
-      thread_regular = thread_regular && (!v || (wt.y != 0.0 && wt2 > 1.000001e-24 * m * m));
+      // Regular: no instance can be degenerate.  |delw| = |wt| / |wdiff| >=
+      // |wt| / (wxmax + |wt|), which exceeds 1e-12 whenever |wt| >= 1e-11
+      // wxmax -- a sqrt-free sufficient condition (the per-item prologue
+      // sits on the critical path of every item).
+      thread_regular = thread_regular && (!v || (wt.y != 0.0 && wt2 >= 1e-22 * p.wxmax * p.wxmax));
     }
     const bool item_regular = __syncthreads_and(!COUNT && thread_regular) != 0;
 
@@ -1003,7 +1005,16 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
       const double wt2 = fma(wt.x, wt.x, wt.y * wt.y);
       const double c1r = e.x * wt.x - e.y * wt.y, c1i = e.x * wt.y + e.y * wt.x;  // eps wt
       const double c2r = e.x * wt2, c2i = e.y * wt2;                              // eps |wt|^2
-      const double rw = item_regular ? (wt2 > 0.0 ? 1.0 / sqrt(wt2) : 0.0) : 1.0;
+      // 1/|wt| from the rsqrt seed and two Newton steps (~1 ulp): the IEEE
+      // sqrt + division would cost more than a band iteration per item.
+      // Regular items have wt2 > 0.
+      double rw = 1.0;
+      if (item_regular) {
+        const double r0 = rsqrt_approx(wt2);
+        const double h = 0.5 * wt2;
+        const double r1 = r0 * fma(-h * r0, r0, 1.5);
+        rw = r1 * fma(-h * r1, r1, 1.5);
+      }
       const double cfr = e.x * rw, cfi = e.y * rw;                                // eps / |wt|
 #pragma unroll
       for (int iw = 0; iw < NW; ++iw) {

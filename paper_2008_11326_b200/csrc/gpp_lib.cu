@@ -172,16 +172,17 @@ struct KernelRef {
   }
 };
 
-// Launch-shape override for experiments: GPP_TUNE="igp,bps" forces the igp
-// tile (2..4) of the rcp_sq kernels at nw 2/3 and caps resident CTAs per SM.
+// Launch-shape override for experiments: GPP_TUNE="igp,bps[,bchunk]" forces
+// the igp tile (2..4) of the ladder rcp_sq kernels at nw 2/3, caps resident
+// CTAs per SM and (optionally) fixes the band chunk.
 // Unset (the default) the planner chooses.
 struct Tune {
-  int igp = 0, bps = 0;
+  int igp = 0, bps = 0, bchunk = 0;
 };
 Tune read_tune() {
   Tune t;
   const char* e = std::getenv("GPP_TUNE");
-  if (e) std::sscanf(e, "%d,%d", &t.igp, &t.bps);
+  if (e) std::sscanf(e, "%d,%d,%d", &t.igp, &t.bps, &t.bchunk);
   return t;
 }
 
@@ -349,8 +350,11 @@ int make_plan_uncached(gpp_ctx* c, int variant, int nw_group, bool count, Plan* 
   pl->blocks_per_sm = std::max(bps, 1);
   if (tune.bps > 0) pl->blocks_per_sm = std::min(pl->blocks_per_sm, tune.bps);
   const long long slots = static_cast<long long>(pl->blocks_per_sm) * c->num_sms;
-  const int bchunk = choose_bchunk(pl->n_igblk, pl->n_igptile, c->nbands, slots,
-                                   fn.sacc ? gpp::kSaccChunk : gpp::kMaxChunk);
+  const int max_chunk = fn.sacc ? gpp::kSaccChunk : gpp::kMaxChunk;
+  const int bchunk = tune.bchunk > 0 ? static_cast<int>(std::min<int64_t>(
+                                           std::min(tune.bchunk, max_chunk), c->nbands))
+                                     : choose_bchunk(pl->n_igblk, pl->n_igptile, c->nbands,
+                                                     slots, max_chunk);
   pl->bchunk = bchunk;
   pl->n_items = static_cast<long long>(pl->n_igblk) * pl->n_igptile *
                 ((c->nbands + bchunk - 1) / bchunk);
