@@ -40,7 +40,7 @@ def src_regs(op, body):
         srcs = args[1:]  # first operand is the destination
     regs = []
     for a in srcs:
-        for m in re.finditer(r"-?\|?R(\d+)(\.reuse)?", a):
+        for m in re.finditer(r"(?<![A-Za-z])R(\d+)(\.reuse)?", a):  # not URn (uniform)
             if "[" in a and op.split(".")[0] in ("LDS", "LDG", "LDC"):
                 pass
             regs.append((int(m.group(1)), bool(m.group(2))))
