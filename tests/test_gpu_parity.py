@@ -260,6 +260,24 @@ def test_pipelined_taper_two_streams(nw):
         ctx.close()
 
 
+@pytest.mark.parametrize("dims,nw", [((600, 3, 40000), 3), ((40, 5, 40000), 2)])
+def test_pipelined_host_evaluate_production_schedules(dims, nw):
+    """The pipelined host path with the production kernel's schedules inside
+    each ig slab: two band windows (600 bands at nw 3) and balanced-tail
+    launches on the other stream (40 bands, several items per CTA)."""
+    p = synth_problem(*dims, seed=9, nw=nw, check=False)
+    want = orc.evaluate_variant(p, "rcp_sq")
+    inst, near, far = orc.branch_stats(p, "rcp_sq")
+    ctx = GPPContext(0)
+    try:
+        for slabs in (0, 1, 5):
+            got, nf, _ = ctx.evaluate_host(p, "rcp_sq", counts=True, slabs=slabs)
+            assert max_rel_error(got, want) <= TOL
+            assert nf == (near, far)
+    finally:
+        ctx.close()
+
+
 @pytest.mark.parametrize("kernel", ["rcp_sq/split", "rcp_sq/iw"])
 def test_ladder_kernels_vs_reference(kernel):
     """The intermediate kernels of the B200 version ladder give the reference's
