@@ -1084,35 +1084,42 @@ __global__ void __launch_bounds__(256) gpp_finalize_kernel(const double* partial
                                                            int fast, int first, int counted,
                                                            double* out,
                                                            unsigned long long* counts) {
-  __shared__ double s[256];
-  __shared__ unsigned long long sc[256];
+  // One coalesced pass: thread t owns column k = t % K of the [nparts][K]
+  // partials and rows t / K, t / K + L, ... (L = 256 / K lanes per column);
+  // the L column sums then add in a fixed order.  Deterministic for a given
+  // nparts, and a single barrier instead of one tree per column.
+  constexpr int K = 4 * NW, L = 256 / K;
+  __shared__ double s[L][K];
+  __shared__ unsigned long long sc[128][2];
   const int tid = threadIdx.x;
-  double sum[4 * NW];
-  for (int k = 0; k < 4 * NW; ++k) {
+  if (tid < L * K) {
+    const int k = tid % K, r0 = tid / K;
     double acc = 0.0;
-    for (int i = tid; i < nparts; i += 256) acc += partials[static_cast<size_t>(i) * 4 * NW + k];
-    s[tid] = acc;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-      if (tid < w) s[tid] += s[tid + w];
-      __syncthreads();
-    }
-    sum[k] = s[0];
-    __syncthreads();
+    for (int i = r0; i < nparts; i += L) acc += partials[static_cast<size_t>(i) * K + k];
+    s[r0][k] = acc;
   }
-  unsigned long long csum[2] = {0ull, 0ull};
-  for (int c = 0; c < 2 && counted; ++c) {
+  if (counted) {
+    const int c = tid & 1, r0 = tid >> 1;
     unsigned long long acc = 0;
-    for (int i = tid; i < nparts; i += 256) acc += cpartials[static_cast<size_t>(i) * 2 + c];
-    sc[tid] = acc;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-      if (tid < w) sc[tid] += sc[tid + w];
-      __syncthreads();
-    }
-    csum[c] = sc[0];
-    __syncthreads();
+    for (int i = r0; i < nparts; i += 128) acc += cpartials[static_cast<size_t>(i) * 2 + c];
+    sc[r0][c] = acc;
   }
+  __syncthreads();
+  __shared__ double s_sum[K];
+  __shared__ unsigned long long s_csum[2];
+  if (tid < K) {
+    double v = 0.0;
+    for (int r = 0; r < L; ++r) v += s[r][tid];
+    s_sum[tid] = v;
+  } else if (tid >= 32 && tid < 34) {
+    unsigned long long v = 0;
+    if (counted)
+      for (int r = 0; r < 128; ++r) v += sc[r][tid - 32];
+    s_csum[tid - 32] = v;
+  }
+  __syncthreads();
+  const double* sum = s_sum;
+  const unsigned long long* csum = s_csum;
   if (tid == 0) {
     for (int iw = 0; iw < NW; ++iw) {
       const double ar = sum[4 * iw + 0], ai = sum[4 * iw + 1];
