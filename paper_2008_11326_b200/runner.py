@@ -132,6 +132,29 @@ class RunArtifacts:
     sim: None = None
 
 
+# Array ids of rooflab's element traces (runner.py:36-46), kept for name
+# compatibility; the trace builders below are out of scope on B200.
+ARRAY_NAMES = {0: "wtilde", 1: "i_eps", 2: "aqsntemp", 3: "aqsmtemp"}
+
+_NO_TRACE = ("element traces model the V100 cache hierarchy for rooflab's cache simulator; "
+             "out of scope on B200 -- profile the kernel with ncu (tools/ncu_summarize.py)")
+
+
+def block_sizes(nbands: int, ncouls: int):
+    """rooflab runner.py:127-136 (trace order helper): not provided."""
+    raise DomainError(_NO_TRACE)
+
+
+def tuple_order(name: str, nbands: int, ngpown: int, ncouls: int):
+    """rooflab runner.py:190-197 (trace order helper): not provided."""
+    raise DomainError(_NO_TRACE)
+
+
+def build_trace(name: str, nbands: int, ngpown: int, ncouls: int):
+    """rooflab runner.py:200-227 (element read trace): not provided."""
+    raise DomainError(_NO_TRACE)
+
+
 def run_version(problem, name: str, trace: bool = False, contraction: bool = True,
                 device: int = 0) -> RunArtifacts:
     """Evaluate one version on the GPU and collect its artifacts (runner.py:249-286)."""
