@@ -65,6 +65,11 @@ SIGNATURES = {
     ),
     "gpp_time": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, _c_float_p, _c_float_p]),
     "gpp_launch_count": (ctypes.c_int, [ctypes.c_void_p, _c_i64_p]),
+    "gpp_plan": (
+        ctypes.c_int,
+        [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+         ctypes.c_int32, _c_i32_p, _c_i64_p],
+    ),
     "gpp_kernel_info": (
         ctypes.c_int,
         [ctypes.c_void_p, ctypes.c_int32, _c_i32_p, _c_i32_p, _c_i32_p, _c_i32_p, _c_i32_p, _c_i32_p],

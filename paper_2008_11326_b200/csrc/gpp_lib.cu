@@ -458,6 +458,25 @@ void split_tail(std::vector<SaccLaunch>& ls, long long slots) {
                 best_bc, R * subs});
 }
 
+// Launches of one ig slab (nblk 256-ig blocks) and one band window [wb0,
+// wb0 + wnb): whole items (band chunk re-planned unless the slab and window
+// are the whole problem, whose plan chunk is `plan_bchunk`), plus the
+// balanced tail for the production kernel.  Pure host logic (gpp_plan).
+std::vector<SaccLaunch> window_launches(int nblk, int n_igptile, int n_igblk_all, int64_t nbands_all,
+                                        int64_t wb0, int64_t wnb, int plan_bchunk, long long slots,
+                                        bool sacc) {
+  const int bchunk = (nblk == n_igblk_all && wnb == nbands_all)
+                         ? plan_bchunk
+                         : choose_bchunk(nblk, n_igptile, wnb, slots,
+                                         sacc ? gpp::kSaccChunk : gpp::kMaxChunk);
+  const int n_rows = nblk * n_igptile;
+  const long long n_chunks = (wnb + bchunk - 1) / bchunk;
+  std::vector<SaccLaunch> launches{{0, n_rows, wb0, wnb, bchunk,
+                                    static_cast<long long>(n_rows) * n_chunks}};
+  if (sacc) split_tail(launches, slots);
+  return launches;
+}
+
 // Optional ig-slab schedule of one evaluation: slab s covers the 256-ig blocks
 // [blk0[s], blk0[s+1]) and its launch waits on ready[s] (the H2D of its rows).
 struct SlabSched {
@@ -517,15 +536,9 @@ int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool
         // A slab (or band window) re-plans its band chunk for its own item
         // count: short chunks keep the last (small) slabs from idling most of
         // the SMs.
-        const int bchunk = (nblk == pl.n_igblk && wnb == c->nbands)
-                               ? pl.bchunk
-                               : choose_bchunk(nblk, pl.n_igptile, wnb, slots,
-                                               fn.sacc ? gpp::kSaccChunk : gpp::kMaxChunk);
-        const int n_rows = nblk * pl.n_igptile;
-        const long long n_chunks = (wnb + bchunk - 1) / bchunk;
-        std::vector<SaccLaunch> launches{{0, n_rows, wb0, wnb, bchunk,
-                                          static_cast<long long>(n_rows) * n_chunks}};
-        if (fn.sacc) split_tail(launches, slots);
+        const std::vector<SaccLaunch> launches =
+            window_launches(nblk, pl.n_igptile, pl.n_igblk, c->nbands, wb0, wnb, pl.bchunk, slots,
+                            fn.sacc != nullptr);
         for (size_t li = 0; li < launches.size(); ++li) {
           const SaccLaunch& L = launches[li];
           cudaStream_t ls = ks;
@@ -989,6 +1002,38 @@ int gpp_time(gpp_ctx* c, int32_t variant, int32_t iters, float* total_ms, float*
   } while (0);
   for (auto& e : evs) cudaEventDestroy(e);
   return result;
+}
+
+int gpp_plan(int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw, int32_t slots,
+             int32_t max_launches, int32_t* n_launches, int64_t* launches) {
+  if (nbands < 1 || ngpown < 1 || ncouls < 1 || nw < 1 || slots < 1 || !n_launches ||
+      (max_launches > 0 && !launches))
+    return fail(GPP_ERR_ARG, "gpp_plan: bad argument");
+  const int nwg = std::min<int>(nw, max_group(GPP_VARIANT_RCP_SQ));
+  const int igp_t = sacc_igp(nwg);
+  const int n_igblk = static_cast<int>((ncouls + gpp::kThreads - 1) / gpp::kThreads);
+  const int n_igptile = static_cast<int>((ngpown + igp_t - 1) / igp_t);
+  const int plan_bchunk = choose_bchunk(n_igblk, n_igptile, nbands, slots, gpp::kSaccChunk);
+  const int64_t win = gpp::kWxParam / nwg;
+  std::vector<SaccLaunch> all;
+  for (int64_t wb0 = 0; wb0 < nbands; wb0 += win) {
+    const std::vector<SaccLaunch> ls = window_launches(
+        n_igblk, n_igptile, n_igblk, nbands, wb0, std::min<int64_t>(win, nbands - wb0),
+        plan_bchunk, slots, true);
+    all.insert(all.end(), ls.begin(), ls.end());
+  }
+  *n_launches = static_cast<int32_t>(all.size());
+  for (int32_t k = 0; k < std::min<int32_t>(max_launches, *n_launches); ++k) {
+    const SaccLaunch& L = all[k];
+    int64_t* o = launches + 6 * k;
+    o[0] = L.row0;
+    o[1] = L.n_rows;
+    o[2] = L.wb0;
+    o[3] = L.wnb;
+    o[4] = L.bchunk;
+    o[5] = L.n_items;
+  }
+  return GPP_OK;
 }
 
 int gpp_launch_count(gpp_ctx* c, int64_t* launches) {

@@ -370,6 +370,20 @@ def evaluate_factored(problem, variant: str = "rcp_sq", device: int = 0) -> GPPR
     return ctx.run_factored(variant, counts=False)[0]
 
 
+def plan_schedule(nbands: int, ngpown: int, ncouls: int, nw: int, slots: int = 296) -> list[dict]:
+    """The production kernel's launches for a whole evaluation (first
+    frequency group) with ``slots`` resident CTAs (gpp_plan; host logic only,
+    no GPU needed): band windows, whole-wave launches and balanced tails."""
+    lib = _lib.load()
+    n = ctypes.c_int32(0)
+    _lib.check(lib.gpp_plan(nbands, ngpown, ncouls, nw, slots, 0, ctypes.byref(n), None), "gpp_plan")
+    out = np.zeros((max(n.value, 1), 6), dtype=np.int64)
+    _lib.check(lib.gpp_plan(nbands, ngpown, ncouls, nw, slots, n.value, ctypes.byref(n),
+                            out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))), "gpp_plan")
+    keys = ("row0", "n_rows", "band0", "nbands", "bchunk", "n_items")
+    return [dict(zip(keys, (int(v) for v in row))) for row in out[: n.value]]
+
+
 def fp64_peak(device: int = 0, iters: int = 200_000) -> tuple[float, float]:
     """Measured FP64 DFMA throughput of the device: (TFLOP/s, ms)."""
     lib = _lib.load()

@@ -1,0 +1,82 @@
+"""The production kernel's launch schedule (csrc/gpp_lib.cu: window_launches,
+split_tail, choose_bchunk) through gpp_plan -- host logic, no GPU needed.
+
+Every (row, band) pair of the problem -- a row being one (256-ig block, igp
+tile) -- must be covered by exactly one item of exactly one launch: the whole
+waves of each band window plus its balanced tail.  The band windows must fit
+the kernel's by-value wx table (kWxParam = 1536 doubles)."""
+import numpy as np
+import pytest
+
+from paper_2008_11326_b200.kernel import plan_schedule
+
+K_WX_PARAM = 1536
+
+
+def _igp_tile(nw: int) -> int:
+    return 2 if min(nw, 3) == 3 else 3
+
+
+def _coverage(nbands, ngpown, ncouls, nw, slots):
+    plan = plan_schedule(nbands, ngpown, ncouls, nw, slots)
+    n_rows = -(-ncouls // 256) * -(-ngpown // _igp_tile(nw))
+    cov = np.zeros((n_rows, nbands), dtype=np.int32)
+    for L in plan:
+        assert 0 <= L["band0"] and L["band0"] + L["nbands"] <= nbands
+        assert L["nbands"] * min(nw, 3) <= K_WX_PARAM
+        assert 1 <= L["bchunk"] <= 256
+        k = np.arange(L["n_items"])
+        chunk, row = k // L["n_rows"], L["row0"] + k % L["n_rows"]
+        assert row.max(initial=0) < n_rows
+        b0 = L["band0"] + chunk * L["bchunk"]
+        b1 = np.minimum(b0 + L["bchunk"], L["band0"] + L["nbands"])
+        assert np.all(b1 > b0)
+        for r, lo, hi in zip(row, b0, b1):
+            cov[r, lo:hi] += 1
+    return plan, cov
+
+
+def test_paper_size_schedule():
+    """(512, 66, 32768) at nw 3 on 296 resident CTAs: 28 whole waves of
+    256-band items, then the last wave's 160 rows in 37-band chunks."""
+    plan = plan_schedule(512, 66, 32768, 3, 296)
+    assert plan == [
+        {"row0": 0, "n_rows": 4224, "band0": 0, "nbands": 512, "bchunk": 256, "n_items": 28 * 296},
+        {"row0": 4224 - 160, "n_rows": 160, "band0": 256, "nbands": 256, "bchunk": 37,
+         "n_items": 160 * 7},
+    ]
+
+
+@pytest.mark.parametrize("dims,nw,slots", [
+    ((512, 66, 32768), 3, 296),
+    ((64, 66, 32768), 3, 296),     # 8-way band shard of the paper size
+    ((600, 7, 5000), 3, 296),      # two band windows
+    ((1100, 5, 3000), 2, 296),
+    ((1600, 4, 2000), 1, 296),
+    ((258, 33, 8192), 3, 296),     # 2-band last chunk
+    ((5, 7, 70000), 3, 296),
+    ((1, 1, 1), 3, 296),
+    ((300, 9, 20000), 2, 100),     # other SM counts
+])
+def test_every_instance_is_scheduled_exactly_once(dims, nw, slots):
+    _, cov = _coverage(*dims, nw, slots)
+    assert cov.min() == 1 and cov.max() == 1
+
+
+def test_random_schedules_cover_exactly_once():
+    rng = np.random.default_rng(0)
+    for _ in range(25):
+        nbands = int(rng.integers(1, 700))
+        ngpown = int(rng.integers(1, 40))
+        ncouls = int(rng.integers(1, 20000))
+        nw = int(rng.integers(1, 5))
+        slots = int(rng.integers(1, 400))
+        _, cov = _coverage(nbands, ngpown, ncouls, nw, slots)
+        assert cov.min() == 1 and cov.max() == 1, (nbands, ngpown, ncouls, nw, slots)
+
+
+def test_tail_only_when_it_shortens_the_modelled_makespan():
+    # A problem whose items are an exact multiple of the resident CTAs has
+    # no partial wave, hence no tail launch.
+    plan = plan_schedule(256, 2, 296 * 256, 3, 296)
+    assert len(plan) == 1 and plan[0]["n_items"] % 296 == 0
