@@ -303,16 +303,50 @@ int choose_igp_tile(int64_t ngpown) {
 // measured at ~4 bands' worth of work (tools/probe_shard.py: step time of
 // 1/N band shards).  Long chunks amortise that cost; short ones balance
 // small shards (and small ig slabs) across the 148 SMs.
+// Modelled cost, in band-steps of one CTA slot, of the balanced tail of a
+// partial last wave (split_tail): R rows of an nb_last-band chunk cut into
+// sub-chunks; 0 in *bc_out when no cut beats one more wave of whole items.
+constexpr double kItemOverheadBands = 4.0;  // measured fixed cost of an item, in bands
+
+double tail_cost(long long R, int64_t nb_last, long long slots, int* bc_out) {
+  double best = static_cast<double>(nb_last) + kItemOverheadBands;
+  *bc_out = 0;
+  for (int64_t k = 2; k <= nb_last; ++k) {
+    const int64_t bc = (nb_last + k - 1) / k, subs = (nb_last + bc - 1) / bc;
+    const long long waves = (R * subs + slots - 1) / slots;
+    const double cost = static_cast<double>(waves) * (static_cast<double>(bc) + kItemOverheadBands);
+    if (cost < best - 0.5) {
+      best = cost;
+      *bc_out = static_cast<int>(bc);
+    }
+  }
+  return best;
+}
+
+bool balanced_tail_enabled();
+
+// Band chunk: minimise the modelled makespan of the static round-robin,
+//   full waves x (chunk + kItemOverheadBands) + the last wave,
+// where the last (partial) wave costs one more whole item, or -- for the
+// production kernel, which balances it (split_tail) -- its tail_cost.  Long
+// chunks amortise the per-item cost (state, staging, barrier, epilogue);
+// short ones balance small shards (and small ig slabs) across the SMs.
 int choose_bchunk(long long n_igblk, long long n_igptile, int64_t nbands, long long slots,
-                  int max_chunk) {
-  constexpr double kItemOverheadBands = 4.0;
+                  int max_chunk, bool balanced) {
+  const long long n_rows = n_igblk * n_igptile;
   int bchunk = 8;
   double best = -1.0;
   for (int bc = 8; bc <= max_chunk; bc *= 2) {
     const int eff = static_cast<int>(std::min<int64_t>(bc, nbands));
-    const long long items = n_igblk * n_igptile * ((nbands + eff - 1) / eff);
-    const long long waves = (items + slots - 1) / slots;
-    const double cost = static_cast<double>(waves) * (eff + kItemOverheadBands);
+    const long long n_chunks = (nbands + eff - 1) / eff;
+    const long long items = n_rows * n_chunks;
+    const long long full = items / slots, R = items % slots;
+    double cost = static_cast<double>((items + slots - 1) / slots) * (eff + kItemOverheadBands);
+    if (balanced && full >= 1 && R > 0 && R <= n_rows) {
+      int bc2 = 0;
+      const int64_t nb_last = nbands - (n_chunks - 1) * eff;
+      cost = static_cast<double>(full) * (eff + kItemOverheadBands) + tail_cost(R, nb_last, slots, &bc2);
+    }
     if (best < 0.0 || cost < best) {
       best = cost;
       bchunk = eff;
@@ -354,7 +388,8 @@ int make_plan_uncached(gpp_ctx* c, int variant, int nw_group, bool count, Plan* 
   const int bchunk = tune.bchunk > 0 ? static_cast<int>(std::min<int64_t>(
                                            std::min(tune.bchunk, max_chunk), c->nbands))
                                      : choose_bchunk(pl->n_igblk, pl->n_igptile, c->nbands,
-                                                     slots, max_chunk);
+                                                     slots, max_chunk,
+                                                     fn.sacc && balanced_tail_enabled());
   pl->bchunk = bchunk;
   pl->n_items = static_cast<long long>(pl->n_igblk) * pl->n_igptile *
                 ((c->nbands + bchunk - 1) / bchunk);
@@ -432,25 +467,14 @@ bool balanced_tail_enabled() {
 }
 
 void split_tail(std::vector<SaccLaunch>& ls, long long slots) {
-  constexpr double kItemOverheadBands = 4.0;
   if (!balanced_tail_enabled()) return;
   const SaccLaunch L = ls[0];
   const long long R = L.n_items % slots, full = L.n_items / slots;
   if (full < 1 || R == 0 || R > L.n_rows) return;
   const int64_t n_chunks = (L.wnb + L.bchunk - 1) / L.bchunk;
   const int64_t last_b0 = (n_chunks - 1) * L.bchunk, nb_last = L.wnb - last_b0;
-  const double base = static_cast<double>(nb_last) + kItemOverheadBands;
-  double best = base;
   int best_bc = 0;
-  for (int64_t k = 2; k <= nb_last; ++k) {
-    const int64_t bc = (nb_last + k - 1) / k, subs = (nb_last + bc - 1) / bc;
-    const long long waves = (R * subs + slots - 1) / slots;
-    const double cost = static_cast<double>(waves) * (static_cast<double>(bc) + kItemOverheadBands);
-    if (cost < best - 0.5) {
-      best = cost;
-      best_bc = static_cast<int>(bc);
-    }
-  }
+  tail_cost(R, nb_last, slots, &best_bc);
   if (best_bc == 0) return;
   ls[0].n_items = full * slots;
   const int64_t subs = (nb_last + best_bc - 1) / best_bc;
@@ -468,7 +492,8 @@ std::vector<SaccLaunch> window_launches(int nblk, int n_igptile, int n_igblk_all
   const int bchunk = (nblk == n_igblk_all && wnb == nbands_all)
                          ? plan_bchunk
                          : choose_bchunk(nblk, n_igptile, wnb, slots,
-                                         sacc ? gpp::kSaccChunk : gpp::kMaxChunk);
+                                         sacc ? gpp::kSaccChunk : gpp::kMaxChunk,
+                                         sacc && balanced_tail_enabled());
   const int n_rows = nblk * n_igptile;
   const long long n_chunks = (wnb + bchunk - 1) / bchunk;
   std::vector<SaccLaunch> launches{{0, n_rows, wb0, wnb, bchunk,
@@ -1013,7 +1038,8 @@ int gpp_plan(int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw, int32_t
   const int igp_t = sacc_igp(nwg);
   const int n_igblk = static_cast<int>((ncouls + gpp::kThreads - 1) / gpp::kThreads);
   const int n_igptile = static_cast<int>((ngpown + igp_t - 1) / igp_t);
-  const int plan_bchunk = choose_bchunk(n_igblk, n_igptile, nbands, slots, gpp::kSaccChunk);
+  const int plan_bchunk = choose_bchunk(n_igblk, n_igptile, nbands, slots, gpp::kSaccChunk,
+                                       balanced_tail_enabled());
   const int64_t win = gpp::kWxParam / nwg;
   std::vector<SaccLaunch> all;
   for (int64_t wb0 = 0; wb0 < nbands; wb0 += win) {
