@@ -39,6 +39,11 @@ constexpr int kMaxChunk = 128;    // bands per item (upper bound)
 #define GPP_SACC_CHUNK 256
 #endif
 constexpr int kSaccChunk = GPP_SACC_CHUNK;  // bands per item of gpp_sacc_kernel (upper bound)
+// Item capacity (bands) of gpp_sacc_kernel's aqsmtemp staging per frequency
+// count: 512 at NW = 3 (104 KB of shared memory per CTA, still two per SM),
+// kSaccChunk otherwise (the NW = 1-2 tiles are three igp wide).
+template <int NW>
+constexpr int sacc_cap() { return NW == 3 ? 2 * kSaccChunk : kSaccChunk; }
 constexpr int kMaxIgpTile = 4;    // igp per thread (upper bound)
 constexpr int kMaxNwGroup = 4;    // frequencies per launch (host loops groups)
 constexpr int kAnDepth = 4;       // aqsntemp bands in flight per thread (cp.async ring)
@@ -668,7 +673,7 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_main_kernel(const Params p) {
 template <int NW, int IGP_T>
 struct SaccSmem {
   double2 an[kAnDepth][kThreads];          // aqsntemp ring, one slot per band in flight
-  double2 am[2][kSaccChunk][IGP_T];        // aqsmtemp[igp tile, band chunk]
+  double2 am[2][sacc_cap<NW>()][IGP_T];    // aqsmtemp[igp tile, band chunk]
   double2 we[2][IGP_T][2][kThreads];       // [buf][j][wtilde | eps][thread]
   double acc[4 * NW][kThreads];            // this thread's ach/asx partials
 };

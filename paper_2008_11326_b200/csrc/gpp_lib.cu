@@ -230,6 +230,8 @@ KernelFn pick_plain(int nw) {
 // whose S sums fit the 128-register budget without spills (ptxas -v).
 // Four-frequency groups keep the one-seed kernel (FastPolicy3): their S sums
 // do not fit beside the ach/asx shared-memory slab.
+int sacc_cap(int nw) { return nw == 3 ? gpp::sacc_cap<3>() : gpp::sacc_cap<1>(); }
+
 int sacc_igp(int nw) { return nw <= 1 ? 3 : (nw == 2 ? 3 : (nw == 3 ? 2 : 3)); }
 
 template <int NW, int IGP_T, bool C>
@@ -384,7 +386,7 @@ int make_plan_uncached(gpp_ctx* c, int variant, int nw_group, bool count, Plan* 
   pl->blocks_per_sm = std::max(bps, 1);
   if (tune.bps > 0) pl->blocks_per_sm = std::min(pl->blocks_per_sm, tune.bps);
   const long long slots = static_cast<long long>(pl->blocks_per_sm) * c->num_sms;
-  const int max_chunk = fn.sacc ? gpp::kSaccChunk : gpp::kMaxChunk;
+  const int max_chunk = fn.sacc ? sacc_cap(nw_group) : gpp::kMaxChunk;
   const int bchunk = tune.bchunk > 0 ? static_cast<int>(std::min<int64_t>(
                                            std::min(tune.bchunk, max_chunk), c->nbands))
                                      : choose_bchunk(pl->n_igblk, pl->n_igptile, c->nbands,
@@ -488,11 +490,10 @@ void split_tail(std::vector<SaccLaunch>& ls, long long slots) {
 // balanced tail for the production kernel.  Pure host logic (gpp_plan).
 std::vector<SaccLaunch> window_launches(int nblk, int n_igptile, int n_igblk_all, int64_t nbands_all,
                                         int64_t wb0, int64_t wnb, int plan_bchunk, long long slots,
-                                        bool sacc) {
+                                        bool sacc, int max_chunk) {
   const int bchunk = (nblk == n_igblk_all && wnb == nbands_all)
                          ? plan_bchunk
-                         : choose_bchunk(nblk, n_igptile, wnb, slots,
-                                         sacc ? gpp::kSaccChunk : gpp::kMaxChunk,
+                         : choose_bchunk(nblk, n_igptile, wnb, slots, max_chunk,
                                          sacc && balanced_tail_enabled());
   const int n_rows = nblk * n_igptile;
   const long long n_chunks = (wnb + bchunk - 1) / bchunk;
@@ -563,7 +564,7 @@ int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool
         // the SMs.
         const std::vector<SaccLaunch> launches =
             window_launches(nblk, pl.n_igptile, pl.n_igblk, c->nbands, wb0, wnb, pl.bchunk, slots,
-                            fn.sacc != nullptr);
+                            fn.sacc != nullptr, fn.sacc ? sacc_cap(nwg) : gpp::kMaxChunk);
         for (size_t li = 0; li < launches.size(); ++li) {
           const SaccLaunch& L = launches[li];
           cudaStream_t ls = ks;
@@ -1038,14 +1039,14 @@ int gpp_plan(int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw, int32_t
   const int igp_t = sacc_igp(nwg);
   const int n_igblk = static_cast<int>((ncouls + gpp::kThreads - 1) / gpp::kThreads);
   const int n_igptile = static_cast<int>((ngpown + igp_t - 1) / igp_t);
-  const int plan_bchunk = choose_bchunk(n_igblk, n_igptile, nbands, slots, gpp::kSaccChunk,
+  const int plan_bchunk = choose_bchunk(n_igblk, n_igptile, nbands, slots, sacc_cap(nwg),
                                        balanced_tail_enabled());
   const int64_t win = gpp::kWxParam / nwg;
   std::vector<SaccLaunch> all;
   for (int64_t wb0 = 0; wb0 < nbands; wb0 += win) {
     const std::vector<SaccLaunch> ls = window_launches(
         n_igblk, n_igptile, n_igblk, nbands, wb0, std::min<int64_t>(win, nbands - wb0),
-        plan_bchunk, slots, true);
+        plan_bchunk, slots, true, sacc_cap(nwg));
     all.insert(all.end(), ls.begin(), ls.end());
   }
   *n_launches = static_cast<int32_t>(all.size());

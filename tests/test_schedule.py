@@ -24,7 +24,7 @@ def _coverage(nbands, ngpown, ncouls, nw, slots):
     for L in plan:
         assert 0 <= L["band0"] and L["band0"] + L["nbands"] <= nbands
         assert L["nbands"] * min(nw, 3) <= K_WX_PARAM
-        assert 1 <= L["bchunk"] <= 256
+        assert 1 <= L["bchunk"] <= (512 if min(nw, 3) == 3 else 256)
         k = np.arange(L["n_items"])
         chunk, row = k // L["n_rows"], L["row0"] + k % L["n_rows"]
         assert row.max(initial=0) < n_rows
@@ -37,13 +37,14 @@ def _coverage(nbands, ngpown, ncouls, nw, slots):
 
 
 def test_paper_size_schedule():
-    """(512, 66, 32768) at nw 3 on 296 resident CTAs: 28 whole waves of
-    256-band items, then the last wave's 160 rows in 37-band chunks."""
+    """(512, 66, 32768) at nw 3 on 296 resident CTAs: 14 whole waves of
+    512-band items (one per (igb, igp tile) row), then the last wave's 80
+    rows in 47-band chunks."""
     plan = plan_schedule(512, 66, 32768, 3, 296)
     assert plan == [
-        {"row0": 0, "n_rows": 4224, "band0": 0, "nbands": 512, "bchunk": 256, "n_items": 28 * 296},
-        {"row0": 4224 - 160, "n_rows": 160, "band0": 256, "nbands": 256, "bchunk": 37,
-         "n_items": 160 * 7},
+        {"row0": 0, "n_rows": 4224, "band0": 0, "nbands": 512, "bchunk": 512, "n_items": 14 * 296},
+        {"row0": 4224 - 80, "n_rows": 80, "band0": 0, "nbands": 512, "bchunk": 47,
+         "n_items": 80 * 11},
     ]
 
 
