@@ -705,14 +705,19 @@ template <int NW, int IGP_T>
 __device__ __forceinline__ void sacc_stage(const Params& p, const SaccItem& it,
                                            SaccSmem<NW, IGP_T>& sm, int buf) {
   const int tid = threadIdx.x;
-  for (int k = tid; k < it.nb * IGP_T; k += kThreads) {
-    const int bb = k / IGP_T, j = k - bb * IGP_T;
-    const int igp = it.igpt * IGP_T + j;
-    if (igp < p.ngpown)
-      cp_async16(&sm.am[buf][bb][j],
-                 p.aqsm + static_cast<size_t>(p.band0 + it.b0 + bb) * p.ngpown + igp);
-    else
-      sm.am[buf][bb][j] = make_double2(0.0, 0.0);
+  // Thread t stages column j = t % IGP_T of bands t / IGP_T, + kThreads /
+  // IGP_T, ...: a fixed igp per thread and a strided walk over the bands.
+  constexpr int kStep = kThreads / IGP_T;
+  const int j = tid % IGP_T, igp = it.igpt * IGP_T + j;
+  if (tid < kStep * IGP_T) {
+    int bb = tid / IGP_T;
+    if (igp < p.ngpown) {
+      const double2* src = p.aqsm + static_cast<size_t>(p.band0 + it.b0 + bb) * p.ngpown + igp;
+      const size_t stride = static_cast<size_t>(kStep) * p.ngpown;
+      for (; bb < it.nb; bb += kStep, src += stride) cp_async16(&sm.am[buf][bb][j], src);
+    } else {
+      for (; bb < it.nb; bb += kStep) sm.am[buf][bb][j] = make_double2(0.0, 0.0);
+    }
   }
   const int igc = sacc_igc(p, it);
 #pragma unroll
