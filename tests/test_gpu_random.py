@@ -76,3 +76,35 @@ def test_random_problems(case):
     part, nfs, _ = ctx.evaluate_host(p, kernel, band_range=br, counts=True, slabs=3)
     assert _err(part, want_shard) <= TOL
     assert nfs == (near, far)
+
+
+@st.composite
+def schedule_problems(draw):
+    """Larger band counts than problems(): several wx-table band windows,
+    512-band items, balanced tails and ragged last chunks, at random."""
+    nb = draw(st.integers(200, 1700))
+    ng = draw(st.integers(1, 6))
+    nc = draw(st.integers(500, 24000))
+    nw = draw(st.integers(1, 5))
+    seed = draw(st.integers(0, 2**31 - 1))
+    banded = draw(st.booleans())
+    p = synth_problem(nb, ng, nc, seed=seed, nw=nw, check=False)
+    if banded:
+        rng = np.random.default_rng(seed)
+        wxb = np.asfortranarray(rng.uniform(1.0, 2.0, size=(nw, nb)))
+        p = GPPProblem(nb, ng, nc, p.wtilde, p.i_eps, p.aqsntemp, p.aqsmtemp, wxb)
+    return p
+
+
+@settings(max_examples=12, deadline=None, derandomize=True, suppress_health_check=list(HealthCheck))
+@given(schedule_problems())
+def test_random_production_schedules(p):
+    want = orc.evaluate_variant(p, "rcp_sq")
+    _, near, far = orc.branch_stats(p, "rcp_sq")
+    ctx = _ctx()
+    ctx.upload(p, force=True)
+    got, nf, _ = ctx.run("rcp_sq", counts=True)
+    assert _err(got, want) <= TOL
+    assert nf == (near, far)
+    fast, _, _ = ctx.run("rcp_sq", counts=False)
+    assert _err(fast, want) <= TOL
