@@ -431,6 +431,9 @@ def run_ours(args, dist: Dist):
         "config": _config(args, dims),
         "roofline": {
             "bound": "fp64",
+            "bound_note": ("the contract's enum is hbm|tensor; this path is bound by the FP64 vector "
+                           "pipe (DFMA): no dense contraction for tensor cores (north star), DRAM at "
+                           "~1.4 % of peak"),
             "achieved": achieved,
             "peak": peak_tf,
             "unit": "TFLOP/s",
