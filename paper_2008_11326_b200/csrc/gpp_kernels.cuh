@@ -15,17 +15,20 @@
 // Work decomposition (one persistent CTA per SM slot, static round-robin
 // items so the reduction order -- and therefore the result -- is
 // deterministic run to run):
-//   item  = (igp tile of IGP_T, ig block of 256, band chunk of <= 64)
+//   item  = (igp tile of IGP_T, ig block of 256, band chunk)
 //   thread <-> ig (coalesced along the F-order ig-fastest arrays); the
 //   IGP_T (ig, igp) states live in registers; the band loop runs innermost
-//   with aqsmtemp[igp tile, band chunk] and wx[band chunk, :] staged in shared
-//   memory (uniform broadcast reads); aqsntemp[ig, band] is streamed from
-//   global through a per-thread cp.async ring kAnDepth bands deep, so its
-//   latency is covered without holding prefetched values in registers.  Items are ordered igp-tile
-//   fastest, so the CTAs resident at one time share the same aqsntemp tile
-//   through L2.
-//   iw is innermost: t and eps*t are formed once per (band, igp, ig) and
+//   with aqsmtemp[igp tile, band chunk] staged in shared memory (uniform
+//   broadcast reads); aqsntemp[ig, band] is streamed from global through a
+//   per-thread cp.async ring kAnDepth bands deep, so its latency is covered
+//   without holding prefetched values in registers.  Items are ordered
+//   igp-tile fastest, so the CTAs resident at one time share the same
+//   aqsntemp tile through L2.
+//   iw is innermost: t = an conj(am) is formed once per (band, igp, ig) and
 //   reused by every frequency from registers (the paper's iw hoist).
+// The production kernel is gpp_sacc_kernel (per-(igp, iw) band sums, wx as a
+// by-value parameter table, cross-item pipelining); the
+// gpp_main_kernel policies are the version-ladder kernels (v0-v7).
 #pragma once
 
 #include <cuda_runtime.h>
