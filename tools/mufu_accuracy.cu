@@ -8,7 +8,8 @@
 #include "gpp_kernels.cuh"
 
 __global__ void acc_kernel(const double* x, int n, double* err) {
-  // err[0..5]: max rel err of rcp.approx, rcp_refined, rsqrt.approx, sqrt_nr<1>, sqrt_nr<2>, mean signed rcp_refined
+  // err[0..6]: max rel err of rcp.approx, rcp_refined, rsqrt.approx, sqrt_nr<1>, sqrt_nr<3>,
+  // and the production step's 1/d and sqrt(d)
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double v = x[i];
@@ -22,10 +23,32 @@ __global__ void acc_kernel(const double* x, int n, double* err) {
   e[2] = fabs(rs - 1.0 / s_exact) * s_exact;
   e[3] = fabs(gpp::sqrt_nr<1>(v) - s_exact) / s_exact;
   e[4] = fabs(gpp::sqrt_nr<3>(v) - s_exact) / s_exact;
-  for (int k = 0; k < 5; ++k) {
+  // The production kernel's step (gpp_kernels.cuh sacc_band): MUFU.RSQ64H
+  // high word paired with an arbitrary (dead) low word, one cubic step, then
+  // 1/d = rr^2 and sqrt(d) = t (1 + q).  The low word here is the element
+  // index, scrambled: any value must do.
+  double r;
+  const double junk = __longlong_as_double(0x3ff0000000000000ull ^ (i * 0x9E3779B97F4A7C15ull));
+  asm("{\n\t.reg .b32 wl, wh, rl, rh;\n\t.reg .f64 s;\n\t"
+      "mov.b64 {wl, wh}, %1;\n\t"
+      "rsqrt.approx.ftz.f64 s, %2;\n\t"
+      "mov.b64 {rl, rh}, s;\n\t"
+      "mov.b64 %0, {wl, rh};\n\t}"
+      : "=d"(r) : "d"(junk), "d"(v));
+  const double t = v * r;
+  const double ee = fma(-t, r, 1.0);
+  const double pe = fma(ee, 0.375, 0.5);
+  const double q = ee * pe;
+  const double rr = fma(r, q, r);
+  const double sq = fma(t, q, t);
+  const double inv = rr * rr;
+  e[5] = fabs(inv - exact_r) / exact_r;
+  double e6 = fabs(sq - s_exact) / s_exact;
+  for (int k = 0; k < 6; ++k) {
     unsigned long long* p = reinterpret_cast<unsigned long long*>(err + k);
     atomicMax(p, __double_as_longlong(e[k]));
   }
+  atomicMax(reinterpret_cast<unsigned long long*>(err + 6), __double_as_longlong(e6));
 }
 
 template <int CH>
@@ -70,13 +93,15 @@ int main() {
     h[i] = std::pow(10.0, -8.0 + 16.0 * u);  // 1e-8 .. 1e8, log-uniform
   }
   double *x, *err;
-  cudaMalloc(&x, n * 8); cudaMalloc(&err, 6 * 8);
+  cudaMalloc(&x, n * 8); cudaMalloc(&err, 8 * 8);
   cudaMemcpy(x, h, n * 8, cudaMemcpyHostToDevice);
-  cudaMemset(err, 0, 6 * 8);
+  cudaMemset(err, 0, 8 * 8);
   acc_kernel<<<(n + 255) / 256, 256>>>(x, n, err);
-  double e[6]; cudaMemcpy(e, err, 6 * 8, cudaMemcpyDeviceToHost);
+  double e[8]; cudaMemcpy(e, err, 8 * 8, cudaMemcpyDeviceToHost);
   printf("max rel err: rcp.approx %.3e (2^%.1f)  rcp_refined %.3e  rsqrt.approx %.3e (2^%.1f)  sqrt_nr1 %.3e  sqrt_nr3(cubic) %.3e\n",
          e[0], std::log2(e[0]), e[1], e[2], std::log2(e[2]), e[3], e[4]);
+  printf("production step (seed high word + arbitrary low word, one cubic step): 1/d %.3e (%.2f ulp)  sqrt(d) %.3e (%.2f ulp)\n",
+         e[5], e[5] / 1.1102230246251565e-16, e[6], e[6] / 1.1102230246251565e-16);
   peak<4>(8, 256); peak<8>(8, 256); peak<16>(8, 256); peak<8>(4, 256); peak<8>(16, 128); peak<32>(4, 256);
   return 0;
 }
