@@ -43,10 +43,10 @@ constexpr int kMaxChunk = 128;    // bands per item (upper bound)
 #endif
 constexpr int kSaccChunk = GPP_SACC_CHUNK;  // bands per item of gpp_sacc_kernel (upper bound)
 // Item capacity (bands) of gpp_sacc_kernel's aqsmtemp staging per frequency
-// count: 512 at NW = 3 (104 KB of shared memory per CTA, still two per SM),
-// kSaccChunk otherwise (the NW = 1-2 tiles are three igp wide).
+// count: 512 at NW = 2-3 (two-igp tiles; 96-104 KB of shared memory per CTA,
+// still two per SM), kSaccChunk at NW = 1 (a three-igp tile).
 template <int NW>
-constexpr int sacc_cap() { return NW == 3 ? 2 * kSaccChunk : kSaccChunk; }
+constexpr int sacc_cap() { return NW >= 2 ? 2 * kSaccChunk : kSaccChunk; }
 constexpr int kMaxIgpTile = 4;    // igp per thread (upper bound)
 constexpr int kMaxNwGroup = 4;    // frequencies per launch (host loops groups)
 constexpr int kAnDepth = 4;       // aqsntemp bands in flight per thread (cp.async ring)

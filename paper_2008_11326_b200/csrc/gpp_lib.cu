@@ -230,9 +230,9 @@ KernelFn pick_plain(int nw) {
 // whose S sums fit the 128-register budget without spills (ptxas -v).
 // Four-frequency groups keep the one-seed kernel (FastPolicy3): their S sums
 // do not fit beside the ach/asx shared-memory slab.
-int sacc_cap(int nw) { return nw == 3 ? gpp::sacc_cap<3>() : gpp::sacc_cap<1>(); }
+int sacc_cap(int nw) { return nw >= 2 ? gpp::sacc_cap<3>() : gpp::sacc_cap<1>(); }
 
-int sacc_igp(int nw) { return nw <= 1 ? 3 : (nw == 2 ? 3 : (nw == 3 ? 2 : 3)); }
+int sacc_igp(int nw) { return nw <= 1 ? 3 : 2; }
 
 template <int NW, int IGP_T, bool C>
 KernelRef sacc_ref() {
@@ -246,7 +246,7 @@ template <bool C>
 KernelRef pick_sacc(int nw) {
   switch (nw) {
     case 1: return sacc_ref<1, 3, C>();
-    case 2: return sacc_ref<2, 3, C>();
+    case 2: return sacc_ref<2, 2, C>();
     case 3: return sacc_ref<3, 2, C>();
     default: {
       KernelRef k;

@@ -14,7 +14,7 @@ K_WX_PARAM = 1536
 
 
 def _igp_tile(nw: int) -> int:
-    return 2 if min(nw, 3) == 3 else 3
+    return 3 if nw == 1 else 2
 
 
 def _coverage(nbands, ngpown, ncouls, nw, slots):
@@ -24,7 +24,7 @@ def _coverage(nbands, ngpown, ncouls, nw, slots):
     for L in plan:
         assert 0 <= L["band0"] and L["band0"] + L["nbands"] <= nbands
         assert L["nbands"] * min(nw, 3) <= K_WX_PARAM
-        assert 1 <= L["bchunk"] <= (512 if min(nw, 3) == 3 else 256)
+        assert 1 <= L["bchunk"] <= (256 if nw == 1 else 512)
         k = np.arange(L["n_items"])
         chunk, row = k // L["n_rows"], L["row0"] + k % L["n_rows"]
         assert row.max(initial=0) < n_rows
