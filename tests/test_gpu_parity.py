@@ -419,3 +419,35 @@ def test_production_schedules_vs_oracle(dims, nw):
     assert max_rel_error(got, want) <= TOL
     assert max_rel_error(evaluate_variant(p, "rcp_sq"), want) <= TOL
     assert (stats.instances, stats.near, stats.far) == (inst, near, far)
+
+
+def test_concurrent_contexts_from_threads():
+    """Independent runs may proceed concurrently: two contexts
+    on the same device, driven from two threads (ctypes releases the GIL),
+    each with its own problem; the by-value wx tables and per-context
+    buffers/streams keep them apart."""
+    import threading
+
+    probs = [synth_problem(300, 5, 9000, seed=s, nw=nw, check=False) for s, nw in ((3, 3), (4, 2))]
+    wants = [orc.evaluate_variant(p, "rcp_sq") for p in probs]
+    errs = [None, None]
+
+    def work(k):
+        ctx = GPPContext(0)
+        try:
+            ctx.upload(probs[k], force=True)
+            worst = 0.0
+            for _ in range(20):
+                got, _, _ = ctx.run("rcp_sq", counts=False)
+                worst = max(worst, max_rel_error(got, wants[k]))
+            errs[k] = worst
+        finally:
+            ctx.close()
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert errs[0] is not None and errs[1] is not None
+    assert max(errs) <= TOL
