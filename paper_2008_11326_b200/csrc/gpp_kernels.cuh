@@ -78,7 +78,14 @@ struct Params {
   unsigned long long rows_mul;
   int rows_shift;
   double wxmax;            // max |wx| over the uploaded bands (regular-item guard)
-  double* partials;                 // [gridDim.x][4 * NW]
+  // gpp_sacc_kernel writes one row of 4 * NW doubles per (item, warp) into the
+  // canonical slot of its (band chunk, row): slot = slot_base + chunk *
+  // slot_stride + row (host: the whole-problem plan numbers every item once,
+  // so every schedule -- resident, ig slabs, any grid -- writes the same
+  // values to the same slots and the finalize sums them in slot order).
+  long long slot_base;
+  int slot_stride;
+  double* partials;                 // [gridDim.x][4 * NW]  (gpp_sacc_kernel: [slot][warp][4 * NW])
   unsigned long long* cpartials;    // [gridDim.x][2]
 };
 
@@ -678,11 +685,11 @@ struct SaccSmem {
   double2 an[kAnDepth][kThreads];          // aqsntemp ring, one slot per band in flight
   double2 am[2][sacc_cap<NW>()][IGP_T];    // aqsmtemp[igp tile, band chunk]
   double2 we[2][IGP_T][2][kThreads];       // [buf][j][wtilde | eps][thread]
-  double acc[4 * NW][kThreads];            // this thread's ach/asx partials
 };
 
 struct SaccItem {
   int igpt, igb, b0, nb;
+  int row, chunk;
 };
 
 __device__ __forceinline__ SaccItem sacc_item(const Params& p, unsigned item) {
@@ -690,6 +697,8 @@ __device__ __forceinline__ SaccItem sacc_item(const Params& p, unsigned item) {
   const unsigned bcu = fastdiv(item, p.rows_mul, p.rows_shift);
   const unsigned row = item - bcu * static_cast<unsigned>(p.n_rows) + static_cast<unsigned>(p.row0);
   const unsigned igb = fastdiv(row, p.igpt_mul, p.igpt_shift);
+  it.row = static_cast<int>(row);
+  it.chunk = static_cast<int>(bcu);
   it.igpt = static_cast<int>(row - igb * p.n_igptile);
   it.igb = static_cast<int>(igb);
   it.b0 = static_cast<int>(bcu) * p.bchunk;
@@ -923,8 +932,7 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
   extern __shared__ __align__(16) unsigned char sacc_smem_raw[];
   SaccSmem<NW, IGP_T>& sm = *reinterpret_cast<SaccSmem<NW, IGP_T>*>(sacc_smem_raw);
   const int tid = threadIdx.x;
-#pragma unroll
-  for (int k = 0; k < 4 * NW; ++k) sm.acc[k][tid] = 0.0;
+  const int lane = tid & 31, warp = tid >> 5;
   Acc<1> cnt;
   cnt.nn = 0;
   cnt.nf = 0;
@@ -1008,7 +1016,7 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
     // the staged buffer: no load latency here).
     double a[4 * NW];
 #pragma unroll
-    for (int k = 0; k < 4 * NW; ++k) a[k] = sm.acc[k][tid];
+    for (int k = 0; k < 4 * NW; ++k) a[k] = 0.0;
 #pragma unroll
     for (int j = 0; j < IGP_T; ++j) {
       const int igp = it.igpt * IGP_T + j;
@@ -1038,8 +1046,18 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
         a[4 * iw + 3] += cfr * f.y + cfi * f.x;
       }
     }
+    // This item's warp partial: xor tree over the lanes (lane 0's fixed
+    // association), one row of 4 * NW doubles into the item's canonical slot.
 #pragma unroll
-    for (int k = 0; k < 4 * NW; ++k) sm.acc[k][tid] = a[k];
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+      for (int k = 0; k < 4 * NW; ++k) a[k] += __shfl_xor_sync(0xffffffffu, a[k], off);
+    if (lane == 0) {
+      const long long slot = p.slot_base + static_cast<long long>(it.chunk) * p.slot_stride + it.row;
+      double2* dst = reinterpret_cast<double2*>(p.partials + (slot * (kThreads / 32) + warp) * (4 * NW));
+#pragma unroll
+      for (int k = 0; k < 2 * NW; ++k) dst[k] = make_double2(a[2 * k], a[2 * k + 1]);
+    }
 
     if (!has_next) break;
     // The staging group (iteration 0) is older than the last kAnDepth - 1
@@ -1052,19 +1070,8 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
   }
   cp_async_wait<0>();
 
-  // CTA reduction straight from sm.acc: warp w sums rows w, w + 8, ... in a
-  // fixed order -- eight strided elements per lane, then an xor tree.
-  __syncthreads();
-  const int lane = tid & 31, warp = tid >> 5;
-  for (int k = warp; k < 4 * NW; k += kThreads / 32) {
-    double v = 0.0;
-#pragma unroll
-    for (int i = 0; i < kThreads / 32; ++i) v += sm.acc[k][lane + 32 * i];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    if (lane == 0) p.partials[static_cast<size_t>(blockIdx.x) * (4 * NW) + k] = v;
-  }
   if constexpr (COUNT) {
+    __syncthreads();
     // The aqsntemp ring is idle now: reuse it for the per-warp counts.
     unsigned long long* s_cnt = reinterpret_cast<unsigned long long*>(&sm.an[0][0]);
     unsigned long long cn = cnt.nn, cf = cnt.nf;
@@ -1078,11 +1085,11 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
       s_cnt[2 * warp + 1] = cf;
     }
     __syncthreads();
-    if (tid < 2) {
+    if (tid < 2) {  // integer counts: one atomic per CTA (order-free, exact)
       unsigned long long sum = 0;
 #pragma unroll
       for (int w = 0; w < kThreads / 32; ++w) sum += s_cnt[2 * w + tid];
-      p.cpartials[static_cast<size_t>(blockIdx.x) * 2 + tid] = sum;
+      atomicAdd(p.cpartials + tid, sum);
     }
   }
 }
@@ -1156,6 +1163,91 @@ __global__ void __launch_bounds__(256) gpp_finalize_kernel(const double* partial
     }
     counts[0] = (first ? 0ull : counts[0]) + csum[0];
     counts[1] = (first ? 0ull : counts[1]) + csum[1];
+  }
+}
+
+// Finalize of the production kernel: sums the canonical (slot, warp) rows in
+// slot order and forms achtemp / asxtemp for the frequency group [iw0, iw0 +
+// NW).  Two stages in one launch: block b sums the slots [b * spb, (b + 1) *
+// spb) (fixed lanes per column, fixed combine order) into stage[b]; the last
+// block to finish (atomic ticket, self-resetting) sums stage[0..gridDim) in
+// order and writes out / counts.  The reduction tree depends only on the slot
+// count, so the result is bitwise the same for every schedule of the items.
+// counts: [near, far] summed from the per-CTA integer rows (any order).
+template <int NW>
+__global__ void __launch_bounds__(256) gpp_slot_finalize_kernel(
+    const double* __restrict__ partials, long long n_slots, int spb, double* stage,
+    unsigned* ticket, const unsigned long long* cpartials, int n_cparts, int nw_total, int iw0,
+    int first, int counted, double* out, unsigned long long* counts) {
+  constexpr int K = 4 * NW, V = (kThreads / 32) * K, L = 256 / V, L2 = 256 / K;
+  __shared__ double s_red[L][V];
+  __shared__ double s_red2[L2][K];
+  __shared__ double s_sum[K];
+  __shared__ unsigned long long sc[128][2];
+  __shared__ unsigned long long s_csum[2];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x;
+  const long long s0 = static_cast<long long>(blockIdx.x) * spb;
+  const long long s1 = min(n_slots, s0 + spb);
+  if (tid < L * V) {
+    const int c = tid % V, l = tid / V;
+    double acc = 0.0;
+    for (long long sl = s0 + l; sl < s1; sl += L) acc += partials[sl * V + c];
+    s_red[l][c] = acc;
+  }
+  __syncthreads();
+  if (tid < K) {
+    double v = 0.0;
+    for (int l = 0; l < L; ++l)
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) v += s_red[l][w * K + tid];
+    stage[static_cast<size_t>(blockIdx.x) * K + tid] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicInc(ticket, gridDim.x - 1) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // Last block: the stage rows in a fixed order (L2 reads: other blocks wrote them).
+  {
+    const int c = tid % K, l = tid / K;
+    if (l < L2) {
+      double acc = 0.0;
+      for (int b = l; b < static_cast<int>(gridDim.x); b += L2)
+        acc += __ldcg(stage + static_cast<size_t>(b) * K + c);
+      s_red2[l][c] = acc;
+    }
+  }
+  if (counted) {
+    const int c = tid & 1, r0 = tid >> 1;
+    unsigned long long acc = 0;
+    for (int i = r0; i < n_cparts; i += 128) acc += cpartials[static_cast<size_t>(i) * 2 + c];
+    sc[r0][c] = acc;
+  }
+  __syncthreads();
+  if (tid < K) {
+    double v = 0.0;
+    for (int l = 0; l < L2; ++l) v += s_red2[l][tid];
+    s_sum[tid] = v;
+  } else if (tid >= 32 && tid < 34) {
+    unsigned long long v = 0;
+    if (counted)
+      for (int r = 0; r < 128; ++r) v += sc[r][tid - 32];
+    s_csum[tid - 32] = v;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int iw = 0; iw < NW; ++iw) {
+      const double ar = s_sum[4 * iw + 0], ai = s_sum[4 * iw + 1];
+      const double br = s_sum[4 * iw + 2], bi = s_sum[4 * iw + 3];
+      out[2 * (iw0 + iw) + 0] = 0.5 * ar;
+      out[2 * (iw0 + iw) + 1] = 0.5 * ai;
+      out[2 * nw_total + 2 * (iw0 + iw) + 0] = fma(-0.25, br, ar);
+      out[2 * nw_total + 2 * (iw0 + iw) + 1] = fma(-0.25, bi, ai);
+    }
+    counts[0] = (first ? 0ull : counts[0]) + s_csum[0];
+    counts[1] = (first ? 0ull : counts[1]) + s_csum[1];
   }
 }
 

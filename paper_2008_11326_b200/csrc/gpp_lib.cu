@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <list>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -81,6 +83,39 @@ struct DevBuf {
   }
 };
 
+// ----- launch planning ------------------------------------------------------
+struct Plan {
+  int igp_t = 4;
+  int bchunk = gpp::kMaxChunk;
+  int n_igblk = 1, n_igptile = 1;
+  long long n_items = 1;
+  int grid = 1;
+  int blocks_per_sm = 1;
+  int regs = 0;
+};
+
+// One launch of the production kernel: rows [row0, row0 + n_rows) of (igb,
+// igp tile) pairs times the band chunks of the window [wb0, wb0 + wnb); the
+// first n_items items (item = chunk * n_rows + row - row0).  `tail`: a
+// balanced-tail launch (run on the other stream).
+struct SaccLaunch {
+  int row0, n_rows;
+  int64_t wb0, wnb;
+  int bchunk;
+  long long n_items;
+  bool tail = false;
+};
+
+struct CanonLaunch : SaccLaunch {
+  long long slot0 = 0;
+};
+struct Canon {
+  Plan pl;
+  int n_rows = 0;
+  std::vector<CanonLaunch> ls;
+  long long n_slots = 0;
+};
+
 }  // namespace
 
 struct gpp_ctx {
@@ -119,6 +154,11 @@ struct gpp_ctx {
   // Launch plans of the uploaded problem, keyed by (variant, nw group, count);
   // cleared whenever a problem is (re)loaded.
   std::vector<std::pair<int, std::vector<int64_t>>> plan_cache;
+  // Canonical schedules of the production kernel, keyed by (nw group, count).
+  std::list<std::pair<int, Canon>> canon_cache;
+  DevBuf<double> stage;      // slot finalize: per-block sums
+  DevBuf<unsigned> ticket;   // slot finalize: last-block ticket (self-resetting)
+  std::mutex mu;             // one caller at a time (the ABI's contexts are shareable)
 
   // ZGEMM-factored path (gpp_run_factored).
   bool wx_band_invariant = false;
@@ -127,6 +167,29 @@ struct gpp_ctx {
 };
 
 namespace {
+
+// One caller at a time per context (the reference allows independent runs to
+// proceed concurrently: distinct contexts run in parallel, a
+// shared one serialises).  Group calls lock every context in address order.
+struct CtxLock {
+  std::vector<std::mutex*> ms;
+  explicit CtxLock(gpp_ctx* c) {
+    if (c) ms.push_back(&c->mu);
+    for (auto* m : ms) m->lock();
+  }
+  CtxLock(gpp_ctx* const* cs, int n) {
+    for (int i = 0; cs && i < n; ++i)
+      if (cs[i]) ms.push_back(&cs[i]->mu);
+    std::sort(ms.begin(), ms.end());
+    ms.erase(std::unique(ms.begin(), ms.end()), ms.end());
+    for (auto* m : ms) m->lock();
+  }
+  ~CtxLock() {
+    for (auto it = ms.rbegin(); it != ms.rend(); ++it) (*it)->unlock();
+  }
+  CtxLock(const CtxLock&) = delete;
+  CtxLock& operator=(const CtxLock&) = delete;
+};
 
 int ensure_init(gpp_ctx* c) {
   if (c->initialized) return GPP_OK;
@@ -150,15 +213,6 @@ int ensure_init(gpp_ctx* c) {
 }
 
 // ----- launch planning ------------------------------------------------------
-struct Plan {
-  int igp_t = 4;
-  int bchunk = gpp::kMaxChunk;
-  int n_igblk = 1, n_igptile = 1;
-  long long n_items = 1;
-  int grid = 1;
-  int blocks_per_sm = 1;
-  int regs = 0;
-};
 
 using KernelFn = void (*)(gpp::Params);
 // The production kernel also takes its band window's wx as a by-value table.
@@ -444,22 +498,14 @@ int nw_groups(int nw, int gmax, std::vector<std::pair<int, int>>* groups) {
   return GPP_OK;
 }
 
-// One launch of the production kernel: rows [row0, row0 + n_rows) of (igb,
-// igp tile) pairs times the band chunks of the window [wb0, wb0 + wnb).
-struct SaccLaunch {
-  int row0, n_rows;
-  int64_t wb0, wnb;
-  int bchunk;
-  long long n_items;
-};
 
 // Balanced tail: the static round-robin leaves the last wave's R items (the
 // last R rows of the last band chunk) on R of the `slots` resident CTAs while
 // the others idle.  If that wave is partial, run the whole waves as one launch
 // and those R rows' last chunk as a second launch cut into finer band chunks,
 // when the modelled makespan (waves x (chunk + per-item overhead)) drops.
-// GPP_BALANCED_TAIL=0 keeps one launch per slab and window: ncu captures of a
-// whole evaluation in one launch (tools/profile_run.py, tools/ladder.py).
+// GPP_BALANCED_TAIL=0 keeps one launch per window: ncu captures of a whole
+// evaluation in one launch (tools/profile_run.py, tools/ladder.py).
 bool balanced_tail_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("GPP_BALANCED_TAIL");
@@ -481,160 +527,327 @@ void split_tail(std::vector<SaccLaunch>& ls, long long slots) {
   ls[0].n_items = full * slots;
   const int64_t subs = (nb_last + best_bc - 1) / best_bc;
   ls.push_back({L.n_rows - static_cast<int>(R), static_cast<int>(R), L.wb0 + last_b0, nb_last,
-                best_bc, R * subs});
+                best_bc, R * subs, true});
 }
 
-// Launches of one ig slab (nblk 256-ig blocks) and one band window [wb0,
-// wb0 + wnb): whole items (band chunk re-planned unless the slab and window
-// are the whole problem, whose plan chunk is `plan_bchunk`), plus the
-// balanced tail for the production kernel.  Pure host logic (gpp_plan).
-std::vector<SaccLaunch> window_launches(int nblk, int n_igptile, int n_igblk_all, int64_t nbands_all,
-                                        int64_t wb0, int64_t wnb, int plan_bchunk, long long slots,
-                                        bool sacc, int max_chunk) {
-  const int bchunk = (nblk == n_igblk_all && wnb == nbands_all)
-                         ? plan_bchunk
-                         : choose_bchunk(nblk, n_igptile, wnb, slots, max_chunk,
-                                         sacc && balanced_tail_enabled());
-  const int n_rows = nblk * n_igptile;
+// Launches of one band window [wb0, wb0 + wnb) over all n_rows rows: whole
+// items plus, for the production kernel, the balanced tail.  Pure host logic.
+std::vector<SaccLaunch> window_launches(int n_rows, int64_t wb0, int64_t wnb, int bchunk,
+                                        long long slots, bool sacc) {
   const long long n_chunks = (wnb + bchunk - 1) / bchunk;
   std::vector<SaccLaunch> launches{{0, n_rows, wb0, wnb, bchunk,
-                                    static_cast<long long>(n_rows) * n_chunks}};
+                                    static_cast<long long>(n_rows) * n_chunks, false}};
   if (sacc) split_tail(launches, slots);
   return launches;
 }
 
-// Optional ig-slab schedule of one evaluation: slab s covers the 256-ig blocks
-// [blk0[s], blk0[s+1]) and its launch waits on ready[s] (the H2D of its rows).
-struct SlabSched {
-  std::vector<int> blk0;             // size S + 1
-  std::vector<cudaEvent_t> ready;    // size S (may be empty: no waits)
+// ----- the canonical schedule of the production kernel -----------------------
+// The whole-problem plan of one frequency group (band windows, each with its
+// whole-wave launch and balanced tail) numbers every item once: the item
+// (chunk, row) of canonical launch L owns slot L.slot0 + chunk * L.n_rows +
+// row - L.row0.  Every schedule that evaluates the problem -- the resident
+// run, the ig-slab pipelined evaluate_host, any grid size -- runs exactly
+// these items (the same band ranges per row) and writes each item's per-warp
+// partial to its slot; the finalize sums the slots in order.  So the result
+// is bitwise the same for every schedule, while each schedule
+// keeps its own launch boundaries and grid.
+
+std::vector<CanonLaunch> canon_launches(int n_igblk, int n_igptile, int64_t nbands, int nwg,
+                                        int plan_bchunk, long long slots, long long* n_slots) {
+  const int64_t win = gpp::kWxParam / nwg;
+  const int n_rows = n_igblk * n_igptile;
+  std::vector<CanonLaunch> all;
+  long long slot = 0;
+  for (int64_t wb0 = 0; wb0 < nbands; wb0 += win) {
+    const int64_t wnb = std::min<int64_t>(win, nbands - wb0);
+    // A window shorter than the whole band range re-plans its band chunk.
+    const int bchunk = wnb == nbands ? plan_bchunk
+                                     : choose_bchunk(n_igblk, n_igptile, wnb, slots, sacc_cap(nwg),
+                                                     balanced_tail_enabled());
+    for (const SaccLaunch& L : window_launches(n_rows, wb0, wnb, bchunk, slots, true)) {
+      CanonLaunch C;
+      static_cast<SaccLaunch&>(C) = L;
+      C.slot0 = slot;
+      slot += L.n_items;
+      all.push_back(C);
+    }
+  }
+  *n_slots = slot;
+  return all;
+}
+
+int make_canon(gpp_ctx* c, int nwg, bool count, const Canon** out) {
+  const int key = nwg * 2 + (count ? 1 : 0);
+  for (const auto& e : c->canon_cache)
+    if (e.first == key) {
+      *out = &e.second;
+      return GPP_OK;
+    }
+  Canon cn;
+  int rc = make_plan(c, GPP_VARIANT_RCP_SQ, nwg, count, &cn.pl);
+  if (rc) return rc;
+  cn.n_rows = cn.pl.n_igblk * cn.pl.n_igptile;
+  const long long slots = static_cast<long long>(cn.pl.blocks_per_sm) * c->num_sms;
+  cn.ls = canon_launches(cn.pl.n_igblk, cn.pl.n_igptile, c->nbands, nwg, cn.pl.bchunk, slots,
+                         &cn.n_slots);
+  c->canon_cache.emplace_back(key, std::move(cn));
+  *out = &c->canon_cache.back().second;
+  return GPP_OK;
+}
+
+// The items of canonical launch L whose rows lie in [r0, r1), as one launch
+// (rows [rr0, rr1), the same chunks; of the last chunk only the rows L runs).
+bool sub_launch(const CanonLaunch& L, int r0, int r1, SaccLaunch* out) {
+  const int rr0 = std::max(r0, L.row0), rr1 = std::min(r1, L.row0 + L.n_rows);
+  if (rr0 >= rr1) return false;
+  const long long n_chunks = (L.wnb + L.bchunk - 1) / L.bchunk;
+  const long long before_last = (n_chunks - 1) * static_cast<long long>(L.n_rows);
+  const long long lim = L.row0 + (L.n_items - before_last);  // rows run in the last chunk
+  const int n = rr1 - rr0;
+  const long long in_last = std::min<long long>(std::max<long long>(lim - rr0, 0), n);
+  *out = {rr0, n, L.wb0, L.wnb, L.bchunk, (n_chunks - 1) * n + in_last, L.tail};
+  return out->n_items > 0;
+}
+
+// ----- one evaluation, enqueued in pieces ------------------------------------
+// eval_begin -> eval_rows(ig blocks [blk0, blk1), after `ready`) ... ->
+// eval_end.  The production kernel runs each piece's canonical items as it
+// is enqueued (pieces alternate between the two compute streams, the tail
+// launches take the other one); the other kernels run the whole problem in
+// eval_end (after every piece's `ready` event), so their partial rows -- and
+// bits -- do not depend on the pieces either.
+struct EvalRun {
+  int variant = 0;
+  bool count = false, sacc = false;
+  std::vector<std::pair<int, int>> groups;
+  std::vector<const Canon*> canon;   // per group (production kernel)
+  std::vector<long long> slot_off;   // per group: first slot in c->partials
+  cudaEvent_t* ev_main = nullptr;
+  int piece = 0;
+  std::vector<cudaEvent_t> pending;  // other kernels: waits deferred to eval_end
 };
 
-// Enqueue one full evaluation on c->stream.  If ev_main is non-null, the
-// main kernels of all frequency groups are bracketed by ev_main[0..1].
-int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool allreduce,
-                 const SlabSched* sched = nullptr) {
-  std::vector<std::pair<int, int>> groups;
-  nw_groups(c->nw, max_group(variant), &groups);
-  const int n_blk_all = static_cast<int>((c->ncouls + gpp::kThreads - 1) / gpp::kThreads);
-  SlabSched whole;
-  whole.blk0 = {0, n_blk_all};
-  const SlabSched& sl = sched ? *sched : whole;
-  const int n_slabs = static_cast<int>(sl.blk0.size()) - 1;
-  bool first = true;
-  for (size_t gi = 0; gi < groups.size(); ++gi) {
-    const int iw0 = groups[gi].first, nwg = groups[gi].second;
-    Plan pl;
-    int rc = make_plan(c, variant, nwg, count, &pl);
-    if (rc) return rc;
-    const KernelRef fn = pick_kernel(variant, nwg, pl.igp_t, count);
-    // The production kernel reads wx from a by-value table, so it runs one
-    // launch per band window of at most kWxParam / nwg bands (one window up
-    // to 512 bands at three frequencies); the other kernels take all bands.
-    const int64_t win = fn.sacc ? gpp::kWxParam / nwg : c->nbands;
-    const int n_win = static_cast<int>((c->nbands + win - 1) / win);
-    if (fn.sacc && pl.n_items >= (1ll << 31))
-      return fail(GPP_ERR_ARG, "too many work items for one launch");
-    // Up to two launches (whole waves + balanced tail) per slab and window.
-    GPP_CUDA(c->partials.ensure(static_cast<size_t>(pl.grid) * n_slabs * n_win * 2 * 4 *
-                                gpp::kMaxNwGroup));
-    GPP_CUDA(c->cpartials.ensure(static_cast<size_t>(pl.grid) * n_slabs * n_win * 2 * 2));
-    int rows = 0;  // partial rows written by this frequency group
-    if (ev_main && gi == 0) GPP_CUDA(cudaEventRecord(ev_main[0], c->stream));
-    // Slabs alternate between two streams so that slab s+1's CTAs fill the
-    // SMs that slab s's last wave leaves idle (each slab writes its own
-    // partial rows; the finalize joins both streams).
-    // (The production kernel also runs its balanced tail launches on the
-    // other stream, where they fill the SMs its whole waves free up.)
-    const bool two = n_slabs > 1 || fn.sacc;
-    if (two) {
-      GPP_CUDA(cudaEventRecord(c->ev_fork, c->stream));
-      GPP_CUDA(cudaStreamWaitEvent(c->kstream2, c->ev_fork, 0));
+constexpr int kSlotsPerFinalizeBlock = 32;
+
+int eval_begin(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, EvalRun* r) {
+  r->variant = variant;
+  r->count = count;
+  r->ev_main = ev_main;
+  nw_groups(c->nw, max_group(variant), &r->groups);
+  r->sacc = variant == GPP_VARIANT_RCP_SQ;
+  if (r->sacc) {
+    long long off = 0, max_slots = 0;
+    size_t doubles = 0;
+    for (const auto& g : r->groups) {
+      const Canon* cn = nullptr;
+      int rc = make_canon(c, g.second, count, &cn);
+      if (rc) return rc;
+      if (cn->n_slots >= (1ll << 31)) return fail(GPP_ERR_ARG, "too many work items");
+      r->canon.push_back(cn);
+      r->slot_off.push_back(off);
+      off += cn->n_slots;
+      max_slots = std::max(max_slots, cn->n_slots);
+      doubles += static_cast<size_t>(cn->n_slots) * (gpp::kThreads / 32) * 4 * g.second;
     }
-    for (int s = 0; s < n_slabs; ++s) {
-      const int nblk = sl.blk0[s + 1] - sl.blk0[s];
-      if (nblk <= 0) continue;
-      cudaStream_t ks = (two && (s & 1)) ? c->kstream2 : c->stream;
-      if (gi == 0 && !sl.ready.empty()) GPP_CUDA(cudaStreamWaitEvent(ks, sl.ready[s], 0));
-      for (int w = 0; w < n_win; ++w) {
-        const int64_t wb0 = w * win, wnb = std::min<int64_t>(win, c->nbands - wb0);
-        const long long slots = static_cast<long long>(pl.blocks_per_sm) * c->num_sms;
-        // A slab (or band window) re-plans its band chunk for its own item
-        // count: short chunks keep the last (small) slabs from idling most of
-        // the SMs.
-        const std::vector<SaccLaunch> launches =
-            window_launches(nblk, pl.n_igptile, pl.n_igblk, c->nbands, wb0, wnb, pl.bchunk, slots,
-                            fn.sacc != nullptr, fn.sacc ? sacc_cap(nwg) : gpp::kMaxChunk);
-        for (size_t li = 0; li < launches.size(); ++li) {
-          const SaccLaunch& L = launches[li];
-          cudaStream_t ls = ks;
-          if (li > 0) {  // balanced tail: independent items, on the other stream
-            ls = ks == c->stream ? c->kstream2 : c->stream;
-            if (gi == 0 && !sl.ready.empty()) GPP_CUDA(cudaStreamWaitEvent(ls, sl.ready[s], 0));
-          }
-          gpp::Params p;
-          p.wtilde = c->wtilde.ptr;
-          p.eps = c->eps.ptr;
-          p.aqsn = c->aqsn.ptr;
-          p.aqsm = c->aqsm.ptr;
-          p.wxb = c->wxb.ptr;
-          p.ncouls = static_cast<int>(c->ncouls);
-          p.ngpown = static_cast<int>(c->ngpown);
-          p.nbands = static_cast<int>(L.wnb);
-          p.band0 = static_cast<int>(L.wb0);
-          p.nw_total = c->nw;
-          p.iw0 = iw0;
-          p.igblk0 = sl.blk0[s];
-          p.n_igblk = nblk;
-          p.n_igptile = pl.n_igptile;
-          p.row0 = L.row0;
-          p.n_rows = L.n_rows;
-          gpp::fastdiv_init(static_cast<unsigned>(p.n_igptile), &p.igpt_mul, &p.igpt_shift);
-          gpp::fastdiv_init(static_cast<unsigned>(p.n_rows), &p.rows_mul, &p.rows_shift);
-          p.bchunk = L.bchunk;
-          p.n_items = L.n_items;
-          p.wxmax = c->wxmax;
-          const int grid = static_cast<int>(std::min<long long>(pl.grid, p.n_items));
-          p.partials = c->partials.ptr + static_cast<size_t>(rows) * 4 * nwg;
-          p.cpartials = c->cpartials.ptr + static_cast<size_t>(rows) * 2;
-          if (fn.sacc) {
-            gpp::WxTable t;
-            for (int64_t b = 0; b < L.wnb; ++b)
-              for (int iw = 0; iw < nwg; ++iw)
-                t.w[b * nwg + iw] = c->h_wx[(L.wb0 + b) * c->nw + iw0 + iw];
-            fn.sacc<<<grid, gpp::kThreads, fn.smem, ls>>>(p, t);
-            ++c->launches;
-          } else {
-            fn.fn<<<grid, gpp::kThreads, 0, ls>>>(p);
-            ++c->launches;
-          }
-          GPP_CUDA(cudaGetLastError());
-          rows += grid;
-        }
-      }
+    GPP_CUDA(c->partials.ensure(doubles));
+    GPP_CUDA(c->cpartials.ensure(2 * r->groups.size()));
+    const size_t g_max = static_cast<size_t>((max_slots + kSlotsPerFinalizeBlock - 1) /
+                                             kSlotsPerFinalizeBlock);
+    GPP_CUDA(c->stage.ensure(g_max * 4 * gpp::kMaxNwGroup));
+    if (!c->ticket.ptr) {
+      GPP_CUDA(c->ticket.ensure(1));
+      GPP_CUDA(cudaMemsetAsync(c->ticket.ptr, 0, sizeof(unsigned), c->stream));
     }
-    if (two) {
-      GPP_CUDA(cudaEventRecord(c->ev_join, c->kstream2));
-      GPP_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
-    }
-    if (ev_main && gi + 1 == groups.size()) GPP_CUDA(cudaEventRecord(ev_main[1], c->stream));
-    ++c->launches;
-    pick_finalize(nwg)<<<1, 256, 0, c->stream>>>(c->partials.ptr, c->cpartials.ptr, rows,
-                                                  c->nw, iw0, variant >= GPP_VARIANT_RCP_SQ,
-                                                  first ? 1 : 0, count ? 1 : 0, c->out.ptr,
-                                                  c->counts.ptr);
-    GPP_CUDA(cudaGetLastError());
-    first = false;
+    if (count)
+      GPP_CUDA(cudaMemsetAsync(c->cpartials.ptr, 0,
+                               2 * r->groups.size() * sizeof(unsigned long long), c->stream));
   }
-  if (allreduce && c->comm && c->nranks > 1) {
-    GPP_NCCL(ncclGroupStart());
-    GPP_NCCL(ncclAllReduce(c->out.ptr, c->out.ptr, 4 * c->nw, ncclDouble, ncclSum, c->comm,
-                           c->stream));
-    GPP_NCCL(ncclAllReduce(c->counts.ptr, c->counts.ptr, 2, ncclUint64, ncclSum, c->comm,
-                           c->stream));
-    GPP_NCCL(ncclGroupEnd());
+  if (ev_main) GPP_CUDA(cudaEventRecord(ev_main[0], c->stream));
+  if (r->sacc) {
+    GPP_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+    GPP_CUDA(cudaStreamWaitEvent(c->kstream2, c->ev_fork, 0));
   }
   return GPP_OK;
+}
+
+int launch_sacc(gpp_ctx* c, const EvalRun& r, size_t gi, const SaccLaunch& L, const CanonLaunch& C,
+                cudaStream_t s) {
+  const int iw0 = r.groups[gi].first, nwg = r.groups[gi].second;
+  const Canon& cn = *r.canon[gi];
+  const KernelRef fn = pick_kernel(GPP_VARIANT_RCP_SQ, nwg, cn.pl.igp_t, r.count);
+  gpp::Params p{};
+  p.wtilde = c->wtilde.ptr;
+  p.eps = c->eps.ptr;
+  p.aqsn = c->aqsn.ptr;
+  p.aqsm = c->aqsm.ptr;
+  p.wxb = c->wxb.ptr;
+  p.ncouls = static_cast<int>(c->ncouls);
+  p.ngpown = static_cast<int>(c->ngpown);
+  p.nbands = static_cast<int>(L.wnb);
+  p.band0 = static_cast<int>(L.wb0);
+  p.nw_total = c->nw;
+  p.iw0 = iw0;
+  p.igblk0 = 0;
+  p.n_igblk = cn.pl.n_igblk;
+  p.n_igptile = cn.pl.n_igptile;
+  p.row0 = L.row0;
+  p.n_rows = L.n_rows;
+  gpp::fastdiv_init(static_cast<unsigned>(p.n_igptile), &p.igpt_mul, &p.igpt_shift);
+  gpp::fastdiv_init(static_cast<unsigned>(p.n_rows), &p.rows_mul, &p.rows_shift);
+  p.bchunk = L.bchunk;
+  p.n_items = L.n_items;
+  p.wxmax = c->wxmax;
+  p.slot_base = r.slot_off[gi] + C.slot0 - C.row0;
+  p.slot_stride = C.n_rows;
+  p.partials = c->partials.ptr;
+  p.cpartials = c->cpartials.ptr + 2 * gi;
+  const long long slots = static_cast<long long>(cn.pl.blocks_per_sm) * c->num_sms;
+  const int grid = static_cast<int>(std::min<long long>(slots, p.n_items));
+  gpp::WxTable t;
+  for (int64_t b = 0; b < L.wnb; ++b)
+    for (int iw = 0; iw < nwg; ++iw) t.w[b * nwg + iw] = c->h_wx[(L.wb0 + b) * c->nw + iw0 + iw];
+  fn.sacc<<<grid, gpp::kThreads, fn.smem, s>>>(p, t);
+  ++c->launches;
+  GPP_CUDA(cudaGetLastError());
+  return GPP_OK;
+}
+
+int eval_rows(gpp_ctx* c, EvalRun* r, int blk0, int blk1, cudaEvent_t ready) {
+  if (!r->sacc) {
+    if (ready) r->pending.push_back(ready);
+    return GPP_OK;
+  }
+  if (blk1 <= blk0) return GPP_OK;
+  cudaStream_t ks = (r->piece & 1) ? c->kstream2 : c->stream;
+  cudaStream_t other = ks == c->stream ? c->kstream2 : c->stream;
+  ++r->piece;
+  bool waited_ks = false, waited_other = false;
+  for (size_t gi = 0; gi < r->groups.size(); ++gi) {
+    const Canon& cn = *r->canon[gi];
+    const int r0 = blk0 * cn.pl.n_igptile, r1 = blk1 * cn.pl.n_igptile;
+    for (const CanonLaunch& C : cn.ls) {
+      SaccLaunch L;
+      if (!sub_launch(C, r0, r1, &L)) continue;
+      cudaStream_t s = L.tail ? other : ks;
+      bool& waited = L.tail ? waited_other : waited_ks;
+      if (ready && !waited) {
+        GPP_CUDA(cudaStreamWaitEvent(s, ready, 0));
+        waited = true;
+      }
+      int rc = launch_sacc(c, *r, gi, L, C, s);
+      if (rc) return rc;
+    }
+  }
+  return GPP_OK;
+}
+
+// The as-written and ladder kernels: the whole problem per frequency group,
+// one partial row per CTA, the single-block finalize.
+int run_plain_group(gpp_ctx* c, const EvalRun& r, size_t gi, bool first) {
+  const int iw0 = r.groups[gi].first, nwg = r.groups[gi].second;
+  Plan pl;
+  int rc = make_plan(c, r.variant, nwg, r.count, &pl);
+  if (rc) return rc;
+  const KernelRef fn = pick_kernel(r.variant, nwg, pl.igp_t, r.count);
+  GPP_CUDA(c->partials.ensure(static_cast<size_t>(pl.grid) * 4 * gpp::kMaxNwGroup));
+  GPP_CUDA(c->cpartials.ensure(static_cast<size_t>(pl.grid) * 2));
+  gpp::Params p{};
+  p.wtilde = c->wtilde.ptr;
+  p.eps = c->eps.ptr;
+  p.aqsn = c->aqsn.ptr;
+  p.aqsm = c->aqsm.ptr;
+  p.wxb = c->wxb.ptr;
+  p.ncouls = static_cast<int>(c->ncouls);
+  p.ngpown = static_cast<int>(c->ngpown);
+  p.nbands = static_cast<int>(c->nbands);
+  p.band0 = 0;
+  p.nw_total = c->nw;
+  p.iw0 = iw0;
+  p.igblk0 = 0;
+  p.n_igblk = pl.n_igblk;
+  p.n_igptile = pl.n_igptile;
+  p.row0 = 0;
+  p.n_rows = pl.n_igblk * pl.n_igptile;
+  p.bchunk = pl.bchunk;
+  p.n_items = pl.n_items;
+  p.wxmax = c->wxmax;
+  p.partials = c->partials.ptr;
+  p.cpartials = c->cpartials.ptr;
+  fn.fn<<<pl.grid, gpp::kThreads, 0, c->stream>>>(p);
+  ++c->launches;
+  GPP_CUDA(cudaGetLastError());
+  if (r.ev_main && gi + 1 == r.groups.size()) GPP_CUDA(cudaEventRecord(r.ev_main[1], c->stream));
+  pick_finalize(nwg)<<<1, 256, 0, c->stream>>>(c->partials.ptr, c->cpartials.ptr, pl.grid, c->nw,
+                                                iw0, r.variant >= GPP_VARIANT_RCP_SQ, first ? 1 : 0,
+                                                r.count ? 1 : 0, c->out.ptr, c->counts.ptr);
+  ++c->launches;
+  GPP_CUDA(cudaGetLastError());
+  return GPP_OK;
+}
+
+using SlotFinalizeFn = void (*)(const double*, long long, int, double*, unsigned*,
+                                const unsigned long long*, int, int, int, int, int, double*,
+                                unsigned long long*);
+SlotFinalizeFn pick_slot_finalize(int nw) {
+  switch (nw) {
+    case 1: return gpp::gpp_slot_finalize_kernel<1>;
+    case 2: return gpp::gpp_slot_finalize_kernel<2>;
+    default: return gpp::gpp_slot_finalize_kernel<3>;
+  }
+}
+
+int eval_end(gpp_ctx* c, EvalRun* r) {
+  if (!r->sacc) {
+    for (cudaEvent_t e : r->pending) GPP_CUDA(cudaStreamWaitEvent(c->stream, e, 0));
+    for (size_t gi = 0; gi < r->groups.size(); ++gi) {
+      int rc = run_plain_group(c, *r, gi, gi == 0);
+      if (rc) return rc;
+    }
+    return GPP_OK;
+  }
+  GPP_CUDA(cudaEventRecord(c->ev_join, c->kstream2));
+  GPP_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  if (r->ev_main) GPP_CUDA(cudaEventRecord(r->ev_main[1], c->stream));
+  for (size_t gi = 0; gi < r->groups.size(); ++gi) {
+    const int iw0 = r->groups[gi].first, nwg = r->groups[gi].second;
+    const long long n_slots = r->canon[gi]->n_slots;
+    const int grid = static_cast<int>((n_slots + kSlotsPerFinalizeBlock - 1) / kSlotsPerFinalizeBlock);
+    const double* part = c->partials.ptr;
+    for (size_t k = 0; k < gi; ++k)
+      part += static_cast<size_t>(r->canon[k]->n_slots) * (gpp::kThreads / 32) * 4 * r->groups[k].second;
+    pick_slot_finalize(nwg)<<<grid, 256, 0, c->stream>>>(
+        part, n_slots, kSlotsPerFinalizeBlock, c->stage.ptr, c->ticket.ptr,
+        c->cpartials.ptr + 2 * gi, 1, c->nw, iw0, gi == 0 ? 1 : 0, r->count ? 1 : 0, c->out.ptr,
+        c->counts.ptr);
+    ++c->launches;
+    GPP_CUDA(cudaGetLastError());
+  }
+  return GPP_OK;
+}
+
+int allreduce_out(gpp_ctx* c) {
+  if (!(c->comm && c->nranks > 1)) return GPP_OK;
+  GPP_NCCL(ncclGroupStart());
+  GPP_NCCL(ncclAllReduce(c->out.ptr, c->out.ptr, 4 * c->nw, ncclDouble, ncclSum, c->comm,
+                         c->stream));
+  GPP_NCCL(ncclAllReduce(c->counts.ptr, c->counts.ptr, 2, ncclUint64, ncclSum, c->comm,
+                         c->stream));
+  GPP_NCCL(ncclGroupEnd());
+  return GPP_OK;
+}
+
+// Enqueue one full evaluation of the resident problem on c->stream.  If
+// ev_main is non-null, the main kernels are bracketed by ev_main[0..1].
+int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool allreduce) {
+  EvalRun r;
+  int rc = eval_begin(c, variant, count, ev_main, &r);
+  if (rc) return rc;
+  const int n_blk = static_cast<int>((c->ncouls + gpp::kThreads - 1) / gpp::kThreads);
+  rc = eval_rows(c, &r, 0, n_blk, nullptr);
+  if (rc) return rc;
+  rc = eval_end(c, &r);
+  if (rc) return rc;
+  return allreduce ? allreduce_out(c) : GPP_OK;
 }
 
 int check_variant(int32_t variant) {
@@ -689,6 +902,8 @@ void gpp_destroy(gpp_ctx* c) {
     c->cpartials.release();
     c->out.release();
     c->counts.release();
+    c->stage.release();
+    c->ticket.release();
     if (c->h_out) cudaFreeHost(c->h_out);
     if (c->h_counts) cudaFreeHost(c->h_counts);
     if (c->h_wx) cudaFreeHost(c->h_wx);
@@ -779,6 +994,7 @@ int prepare(gpp_ctx* c, const HostProblem& h) {
     invariant = c->h_wx[k] == c->h_wx[k % h.nw];
   c->wx_band_invariant = invariant;
   c->plan_cache.clear();
+  c->canon_cache.clear();
   c->nbands = nb;
   c->ngpown = h.ngpown;
   c->ncouls = h.ncouls;
@@ -820,17 +1036,17 @@ int copy_rows(gpp_ctx* c, const HostProblem& h, int64_t i0, int64_t i1, cudaStre
   return GPP_OK;
 }
 
-// ig-slab schedule of the pipelined evaluate, as block offsets.  slabs > 0:
-// that many equal slabs.  slabs <= 0: a taper -- slab sizes shrink by 1/1.2
-// towards the end, down to single 256-ig blocks.  The copy is the critical
-// path (PCIe ~55 GB/s vs the kernel's ~0.8 of that time); what follows the
-// last byte is the kernel on the last slab, so it should be small, while
-// every earlier slab's kernel must fit inside the next slab's copy (ratio
-// >= 0.8) and the slab count stays low (each 2D copy row costs ~20 ns).
-// tools/probe_slabs.py: 6.43 ms end to end at paper size vs 6.74 ms for 16
-// equal slabs.  GPP_SLABS="b0,b1,..." (block counts summing to the block
-// total) overrides, for experiments.
-std::vector<int> slab_schedule(int n_blk, int slabs) {
+// ig-slab schedule of the pipelined evaluate, as block offsets.  The copy is
+// the critical path (PCIe ~55 GB/s against the kernel's ~0.65 of that time);
+// slab s's items run while slab s+1 is in flight, and what follows the last
+// byte is the last slab's items.  The production kernel runs canonical items
+// (whole rows of up to 512 bands, the balanced tail's last rows in short
+// chunks), so the default is slabs of about one wave of rows (resident CTAs /
+// igp tiles blocks) and a last slab of the blocks whose rows are all
+// balanced-tail rows (short items: little work after the last byte).
+// slabs > 0: that many equal slabs.  GPP_SLABS="b0,b1,..." (block counts
+// summing to the block total) overrides, for experiments.
+std::vector<int> slab_schedule(gpp_ctx* c, const EvalRun& r, int n_blk, int slabs) {
   std::vector<int> sizes;
   if (const char* e = std::getenv("GPP_SLABS")) {
     int sum = 0;
@@ -851,20 +1067,29 @@ std::vector<int> slab_schedule(int n_blk, int slabs) {
                                        static_cast<int64_t>(n_blk) * i / n));
   }
   if (sizes.empty()) {
-    // Built from the end: 1, 1, 2, 3, 4, 5, 6, 8, 10, 12, 15, 18, 22, ...
-    std::vector<int> rev{1};
-    int sum = 1, sz = 1;
-    if (n_blk > 1) {
-      rev.push_back(1);
-      sum = 2;
+    int per = 8, tail_blocks = 0;
+    if (r.sacc && !r.canon.empty()) {
+      const Canon& cn = *r.canon[0];
+      const long long slots = static_cast<long long>(cn.pl.blocks_per_sm) * c->num_sms;
+      per = static_cast<int>(std::max<long long>(1, slots / cn.pl.n_igptile));
+      int first_tail_row = cn.n_rows;
+      for (const CanonLaunch& L : cn.ls)
+        if (L.tail) first_tail_row = std::min(first_tail_row, L.row0);
+      tail_blocks = cn.n_rows - ((first_tail_row + cn.pl.n_igptile - 1) / cn.pl.n_igptile) *
+                                    cn.pl.n_igptile;
+      tail_blocks = std::max(0, tail_blocks / cn.pl.n_igptile);
+    }
+    std::vector<int> rev;
+    int sum = 0;
+    if (tail_blocks > 0 && tail_blocks < n_blk) {
+      rev.push_back(tail_blocks);
+      sum = tail_blocks;
     }
     while (sum < n_blk) {
-      sz = std::max(sz + 1, static_cast<int>(std::ceil(sz * 1.2)));
+      const int sz = std::min(per, n_blk - sum);
       rev.push_back(sz);
       sum += sz;
     }
-    rev.back() -= sum - n_blk;  // the first slab takes the remainder
-    if (rev.back() <= 0) rev.pop_back();
     sizes.assign(rev.rbegin(), rev.rend());
   }
   std::vector<int> blk0{0};
@@ -873,14 +1098,8 @@ std::vector<int> slab_schedule(int n_blk, int slabs) {
 }
 
 int finish_run(gpp_ctx* c, double* achtemp, double* asxtemp, int64_t* near_far) {
-  if (c->comm && c->nranks > 1) {
-    GPP_NCCL(ncclGroupStart());
-    GPP_NCCL(ncclAllReduce(c->out.ptr, c->out.ptr, 4 * c->nw, ncclDouble, ncclSum, c->comm,
-                           c->stream));
-    GPP_NCCL(ncclAllReduce(c->counts.ptr, c->counts.ptr, 2, ncclUint64, ncclSum, c->comm,
-                           c->stream));
-    GPP_NCCL(ncclGroupEnd());
-  }
+  int rc = allreduce_out(c);
+  if (rc) return rc;
   GPP_CUDA(cudaMemcpyAsync(c->h_out, c->out.ptr, 4 * sizeof(double) * c->nw,
                            cudaMemcpyDeviceToHost, c->stream));
   GPP_CUDA(cudaMemcpyAsync(c->h_counts, c->counts.ptr, 2 * sizeof(unsigned long long),
@@ -903,6 +1122,7 @@ int gpp_upload(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32
                const double* wtilde, const double* i_eps, const double* aqsntemp,
                const double* aqsmtemp, const double* wx, int32_t wx_band_indexed,
                int64_t band0, int64_t band1) {
+  CtxLock lock(c);
   const HostProblem h{nbands, ngpown, ncouls, nw, wtilde, i_eps, aqsntemp, aqsmtemp, wx,
                       wx_band_indexed, band0, band1};
   int rc = validate(c, h);
@@ -929,6 +1149,7 @@ int gpp_evaluate_host(gpp_ctx* c, int32_t variant, int64_t nbands, int64_t ngpow
                       const double* aqsntemp, const double* aqsmtemp, const double* wx,
                       int32_t wx_band_indexed, int64_t band0, int64_t band1, int32_t slabs,
                       double* achtemp, double* asxtemp, int64_t* near_far, float* ms) {
+  CtxLock lock(c);
   const HostProblem h{nbands, ngpown, ncouls, nw, wtilde, i_eps, aqsntemp, aqsmtemp, wx,
                       wx_band_indexed, band0, band1};
   int rc = validate(c, h);
@@ -943,31 +1164,32 @@ int gpp_evaluate_host(gpp_ctx* c, int32_t variant, int64_t nbands, int64_t ngpow
   c->have_problem = false;
   rc = prepare(c, h);
   if (rc) return rc;
-  // ig slabs on 256-ig block boundaries.
+  // ig slabs on 256-ig block boundaries; the canonical items of slab s run as
+  // soon as its rows have landed, while slab s+1 is in flight.
   const int n_blk = static_cast<int>((ncouls + gpp::kThreads - 1) / gpp::kThreads);
-  SlabSched sched;
-  sched.blk0 = slab_schedule(n_blk, slabs);
-  const int n_sched = static_cast<int>(sched.blk0.size()) - 1;
+  EvalRun r;
+  rc = eval_begin(c, variant, near_far != nullptr, nullptr, &r);
+  if (rc) return rc;
+  const std::vector<int> blk0 = slab_schedule(c, r, n_blk, slabs);
+  const int n_sched = static_cast<int>(blk0.size()) - 1;
   while (static_cast<int>(c->slab_ev.size()) < n_sched + 1) {
     cudaEvent_t e;
     GPP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c->slab_ev.push_back(e);
   }
-  // Copy stream: small arrays, then the ig rows slab by slab, each slab
-  // signalling the compute streams (two, alternating); slab s computes while
-  // the rows of slab s+1 are in flight.
   GPP_CUDA(cudaEventRecord(c->ev[2], c->cstream));
   rc = copy_small(c, h, c->cstream);
   if (rc) return rc;
   for (int sl = 0; sl < n_sched; ++sl) {
-    const int64_t i0 = static_cast<int64_t>(sched.blk0[sl]) * gpp::kThreads;
-    const int64_t i1 = std::min<int64_t>(ncouls, static_cast<int64_t>(sched.blk0[sl + 1]) * gpp::kThreads);
+    const int64_t i0 = static_cast<int64_t>(blk0[sl]) * gpp::kThreads;
+    const int64_t i1 = std::min<int64_t>(ncouls, static_cast<int64_t>(blk0[sl + 1]) * gpp::kThreads);
     rc = copy_rows(c, h, i0, i1, c->cstream);
     if (rc) return rc;
     GPP_CUDA(cudaEventRecord(c->slab_ev[sl], c->cstream));
-    sched.ready.push_back(c->slab_ev[sl]);
+    rc = eval_rows(c, &r, blk0[sl], blk0[sl + 1], c->slab_ev[sl]);
+    if (rc) return rc;
   }
-  rc = enqueue_eval(c, variant, near_far != nullptr, nullptr, false, &sched);
+  rc = eval_end(c, &r);
   if (rc) return rc;
   GPP_CUDA(cudaEventRecord(c->ev[3], c->stream));
   rc = finish_run(c, achtemp, asxtemp, near_far);
@@ -979,6 +1201,7 @@ int gpp_evaluate_host(gpp_ctx* c, int32_t variant, int64_t nbands, int64_t ngpow
 
 int gpp_run(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp, int64_t* near_far,
             float* kernel_ms) {
+  CtxLock lock(c);
   if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
   int rc = check_variant(variant);
   if (rc) return rc;
@@ -997,6 +1220,7 @@ int gpp_run(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp, int64
 }
 
 int gpp_time(gpp_ctx* c, int32_t variant, int32_t iters, float* total_ms, float* main_ms) {
+  CtxLock lock(c);
   if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
   int rc = check_variant(variant);
   if (rc) return rc;
@@ -1041,17 +1265,12 @@ int gpp_plan(int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw, int32_t
   const int n_igptile = static_cast<int>((ngpown + igp_t - 1) / igp_t);
   const int plan_bchunk = choose_bchunk(n_igblk, n_igptile, nbands, slots, sacc_cap(nwg),
                                        balanced_tail_enabled());
-  const int64_t win = gpp::kWxParam / nwg;
-  std::vector<SaccLaunch> all;
-  for (int64_t wb0 = 0; wb0 < nbands; wb0 += win) {
-    const std::vector<SaccLaunch> ls = window_launches(
-        n_igblk, n_igptile, n_igblk, nbands, wb0, std::min<int64_t>(win, nbands - wb0),
-        plan_bchunk, slots, true, sacc_cap(nwg));
-    all.insert(all.end(), ls.begin(), ls.end());
-  }
+  long long n_slots = 0;
+  const std::vector<CanonLaunch> all =
+      canon_launches(n_igblk, n_igptile, nbands, nwg, plan_bchunk, slots, &n_slots);
   *n_launches = static_cast<int32_t>(all.size());
   for (int32_t k = 0; k < std::min<int32_t>(max_launches, *n_launches); ++k) {
-    const SaccLaunch& L = all[k];
+    const CanonLaunch& L = all[k];
     int64_t* o = launches + 6 * k;
     o[0] = L.row0;
     o[1] = L.n_rows;
@@ -1064,6 +1283,7 @@ int gpp_plan(int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw, int32_t
 }
 
 int gpp_launch_count(gpp_ctx* c, int64_t* launches) {
+  CtxLock lock(c);
   if (!c || !launches) return fail(GPP_ERR_ARG, "ctx / launches is NULL");
   *launches = static_cast<int64_t>(c->launches);
   return GPP_OK;
@@ -1072,6 +1292,7 @@ int gpp_launch_count(gpp_ctx* c, int64_t* launches) {
 int gpp_kernel_info(gpp_ctx* c, int32_t variant, int32_t* registers_per_thread,
                     int32_t* threads_per_block, int32_t* blocks_per_sm, int32_t* grid,
                     int32_t* igp_tile, int32_t* band_chunk) {
+  CtxLock lock(c);
   if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
   int rc = check_variant(variant);
   if (rc) return rc;
@@ -1100,6 +1321,7 @@ int gpp_comm_unique_id(unsigned char* id128) {
 }
 
 int gpp_comm_init(gpp_ctx* c, int nranks, int rank, const unsigned char* id128) {
+  CtxLock lock(c);
   if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
   if (!id128) return fail(GPP_ERR_ARG, "id buffer is NULL");
   if (nranks < 1 || rank < 0 || rank >= nranks)
@@ -1124,6 +1346,7 @@ int gpp_comm_init(gpp_ctx* c, int nranks, int rank, const unsigned char* id128) 
 
 int gpp_synth(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw,
               const uint64_t* pcg_state, const double* wx, int64_t band0, int64_t band1) {
+  CtxLock lock(c);
   if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
   if (!pcg_state || !wx) return fail(GPP_ERR_ARG, "pcg_state / wx is NULL");
   // Validate like an upload (the array pointers are not used).
@@ -1178,6 +1401,7 @@ int gpp_synth(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32_
 
 int gpp_run_factored(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp,
                      int64_t* near_far, float* ms) {
+  CtxLock lock(c);
   if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
   if (variant < GPP_VARIANT_DIV || variant > GPP_VARIANT_RCP_SQ)
     return fail(GPP_ERR_ARG, "the factored path takes a reference variant (0=div, 1=rcp, 2=rcp_sq)");
@@ -1251,6 +1475,7 @@ int gpp_run_factored(gpp_ctx* c, int32_t variant, double* achtemp, double* asxte
 
 int gpp_variant_terms(gpp_ctx* c, int32_t variant, double* sch, double* ssx, uint8_t* near_mask,
                       uint8_t* far_mask) {
+  CtxLock lock(c);
   if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
   if (variant < GPP_VARIANT_DIV || variant > GPP_VARIANT_RCP_SQ)
     return fail(GPP_ERR_ARG, "variant_terms takes a reference variant (0=div, 1=rcp, 2=rcp_sq)");
@@ -1298,6 +1523,7 @@ int gpp_variant_terms(gpp_ctx* c, int32_t variant, double* sch, double* ssx, uin
 }
 
 int gpp_comm_init_all(gpp_ctx** ctxs, int n) {
+  CtxLock lock(ctxs, n);
   if (!ctxs || n < 1) return fail(GPP_ERR_ARG, "need at least one context");
   std::vector<int> devs(n);
   for (int i = 0; i < n; ++i) {
@@ -1327,6 +1553,7 @@ int gpp_comm_init_all(gpp_ctx** ctxs, int n) {
 
 int gpp_run_group(gpp_ctx** ctxs, int n, int32_t variant, double* achtemp, double* asxtemp,
                   int64_t* near_far, float* kernel_ms) {
+  CtxLock lock(ctxs, n);
   if (!ctxs || n < 1) return fail(GPP_ERR_ARG, "need at least one context");
   int rc = check_variant(variant);
   if (rc) return rc;

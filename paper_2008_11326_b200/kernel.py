@@ -8,14 +8,24 @@ evaluates the literal nest formulation (problem.py:179-208, the ``div``
 arithmetic) on the GPU.
 
 ``GPPContext`` is the device-buffer manager: one library context per CUDA
-device; inputs are uploaded once and re-used while the caller keeps passing
-the same read-only arrays (the reference marks synthesized arrays read-only,
-problem.py:154-155).  Writeable arrays are re-uploaded on every call.
+device and calling thread; inputs are uploaded once and re-used while the
+caller keeps passing the same read-only arrays (the reference marks
+synthesized arrays read-only, problem.py:154-155).  Writeable arrays are
+re-uploaded on every call.
+
+Reproducibility and concurrency: every evaluation of the same
+inputs and variant returns the same bits -- the first call (upload pipelined
+with the kernel) and later calls on the resident problem run the same
+canonical items and sum them in the same order -- and
+independent runs may proceed concurrently: each thread gets its own context
+(``get_context``), and a context shared explicitly between threads serialises
+its callers (a lock here and one in the library).
 """
 
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 
@@ -76,6 +86,9 @@ class GPPContext:
     def __init__(self, device: int = 0):
         self._lib = _lib.load()
         self.device = int(device)
+        # Guards the Python-side cache state; the library serialises callers of
+        # one context too (gpp_lib.cu CtxLock).
+        self.lock = threading.RLock()
         handle = ctypes.c_void_p()
         _lib.check(self._lib.gpp_create(ctypes.byref(handle), self.device), "gpp_create")
         self._h = handle
@@ -279,23 +292,32 @@ def comm_unique_id() -> bytes:
     return buf.raw
 
 
-_CONTEXTS: dict[int, GPPContext] = {}
+_TLS = threading.local()
 
 
 def get_context(device: int = 0) -> GPPContext:
-    ctx = _CONTEXTS.get(device)
+    """The calling thread's context on ``device`` (created on first use).
+    Per-thread contexts let independent runs proceed concurrently
+     without sharing device buffers."""
+    ctxs = getattr(_TLS, "contexts", None)
+    if ctxs is None:
+        ctxs = _TLS.contexts = {}
+    ctx = ctxs.get(device)
     if ctx is None:
-        ctx = _CONTEXTS[device] = GPPContext(device)
+        ctx = ctxs[device] = GPPContext(device)
     return ctx
 
 
 def evaluate(problem, variant: str = "rcp_sq", device: int = 0, counts: bool = True):
-    """Upload (cached) + run: (GPPResult, BranchStats | None, kernel_ms)."""
+    """Upload (cached) + run: (GPPResult, BranchStats | None, kernel_ms).
+    The first sight of a problem pipelines its upload with the evaluation
+    (gpp_evaluate_host); both paths return the same bits."""
     ctx = get_context(device)
-    if ctx.is_resident(problem):
-        result, nf, ms = ctx.run(variant, counts=counts)
-    else:  # first sight of these arrays: pipelined upload + evaluation
-        result, nf, ms = ctx.evaluate_host(problem, variant, counts=counts)
+    with ctx.lock:
+        if ctx.is_resident(problem):
+            result, nf, ms = ctx.run(variant, counts=counts)
+        else:
+            result, nf, ms = ctx.evaluate_host(problem, variant, counts=counts)
     stats = None
     if nf is not None:
         nb, ng, nc = ctx.dims
@@ -333,6 +355,11 @@ def variant_terms(problem, variant: str, device: int = 0) -> VariantTerms:
     computed on the GPU; arrays of shape (nw, ncouls, ngpown)."""
     _reference_variant(variant)
     ctx = get_context(device)
+    with ctx.lock:
+        return _variant_terms(ctx, problem, variant)
+
+
+def _variant_terms(ctx, problem, variant):
     ctx.upload(problem)
     nw, nc, ng = ctx.nw, int(problem.ncouls), int(problem.ngpown)
     sch = np.empty((nw, nc, ng), dtype=np.complex128)
@@ -366,8 +393,9 @@ def evaluate_factored(problem, variant: str = "rcp_sq", device: int = 0) -> GPPR
     for band-invariant wx; evaluate_variant runs the per-instance nest."""
     _reference_variant(variant)
     ctx = get_context(device)
-    ctx.upload(problem)
-    return ctx.run_factored(variant, counts=False)[0]
+    with ctx.lock:
+        ctx.upload(problem)
+        return ctx.run_factored(variant, counts=False)[0]
 
 
 def plan_schedule(nbands: int, ngpown: int, ncouls: int, nw: int, slots: int = 296) -> list[dict]:

@@ -123,7 +123,7 @@ class RunArtifacts:
     counters: InstructionCounters
     stats: BranchStats
     elapsed_s: float          # wall time of the evaluation call (perf_counter)
-    kernel_s: float           # device time of the compute kernels (CUDA events)
+    kernel_s: float           # device time of the evaluation (CUDA events)
     registers_per_thread: int
     threads_per_block: int
     occupancy: OccupancyResult
@@ -155,21 +155,8 @@ def build_trace(name: str, nbands: int, ngpown: int, ncouls: int):
     raise DomainError(_NO_TRACE)
 
 
-def run_version(problem, name: str, trace: bool = False, contraction: bool = True,
-                device: int = 0) -> RunArtifacts:
-    """Evaluate one version on the GPU and collect its artifacts (runner.py:249-286)."""
+def _artifacts(ctx, problem, name, kernel, result, kernel_ms, elapsed, contraction) -> RunArtifacts:
     spec = version_spec(name)
-    if trace:
-        raise DomainError("element traces belong to rooflab's cache model; profile with ncu instead")
-    ctx = get_context(device)
-    # Timed like the reference (runner.py:258-260): the evaluation alone; the
-    # branch statistics come from a second, counting launch (kernel.py:262
-    # computes them in a separate pass too).
-    kernel = B200_KERNEL[name]
-    start = time.perf_counter()
-    ctx.upload(problem)
-    result, _, kernel_ms = ctx.run(kernel, counts=False)
-    elapsed = time.perf_counter() - start
     _, (near, far), _ = ctx.run(spec.variant, counts=True)
     nb, ng, nc = ctx.dims
     tuples = nb * ng * nc
@@ -193,6 +180,50 @@ def run_version(problem, name: str, trace: bool = False, contraction: bool = Tru
         occupancy=OccupancyResult(warps=min(warps, 64), blocks=info["blocks_per_sm"]),
         description=spec.description,
     )
+
+
+def run_version(problem, name: str, trace: bool = False, contraction: bool = True,
+                device: int = 0) -> RunArtifacts:
+    """Evaluate one version on the GPU and collect its artifacts (runner.py:249-286).
+
+    As in the reference, the result comes from the version's *variant* alone
+    (runner.py:258-260 calls evaluate_variant(problem, spec.variant)): every
+    version sharing a variant returns bit-identical accumulators
+    (test_gpp.py:88-94) -- v3..v8 all run the rcp_sq production kernel.  The
+    paper's per-step kernels are ``run_ladder``.
+    """
+    spec = version_spec(name)
+    if trace:
+        raise DomainError("element traces belong to rooflab's cache model; profile with ncu instead")
+    ctx = get_context(device)
+    with ctx.lock:
+        # Timed like the reference (runner.py:258-260): the evaluation alone;
+        # the branch statistics come from a second, counting launch
+        # (kernel.py:262 computes them in a separate pass too).
+        start = time.perf_counter()
+        if ctx.is_resident(problem):
+            result, _, kernel_ms = ctx.run(spec.variant, counts=False)
+        else:
+            result, _, kernel_ms = ctx.evaluate_host(problem, spec.variant)
+        elapsed = time.perf_counter() - start
+        return _artifacts(ctx, problem, name, spec.variant, result, kernel_ms, elapsed, contraction)
+
+
+def run_ladder(problem, name: str, contraction: bool = True, device: int = 0) -> RunArtifacts:
+    """The B200 version ladder: version ``name``'s optimisation step
+    re-derived as its own sm_100a kernel (B200_KERNEL) --
+    the per-step evidence of the paper's trajectory.  Results agree with the
+    reference to rounding (not bitwise across versions: the kernels' FP64
+    arithmetic differs); counters are the reference's for the version."""
+    version_spec(name)
+    kernel = B200_KERNEL[name]
+    ctx = get_context(device)
+    with ctx.lock:
+        ctx.upload(problem)
+        start = time.perf_counter()
+        result, _, kernel_ms = ctx.run(kernel, counts=False)
+        elapsed = time.perf_counter() - start
+        return _artifacts(ctx, problem, name, kernel, result, kernel_ms, elapsed, contraction)
 
 
 def run_sweep(problem, names=None, device: int = 0) -> list[RunArtifacts]:

@@ -16,7 +16,10 @@ three modules that import it by value (SURVEY.md Table R).
 ``--big`` adds the paper size (512, 66, 32768) and the weak-scaled size
 (4096, 528, 65536); the weak case needs ~18 GB of RAM and ~1 minute.
 ``--append weak-nw3`` adds the weak size at nw = 3 (the bench default) to an
-existing gpp_big.json.
+existing gpp_big.json.  ``--append sweep`` adds every point of the igp/ig
+aspect-ratio sweep (BASELINE.json configs[4]: nbands 512, ngpown in
+SWEEP_NGPOWN x ncouls in SWEEP_NCOULS, seed 1, nw 3) that gpp_big.json does
+not hold yet.
 """
 
 from __future__ import annotations
@@ -40,6 +43,8 @@ HERE = Path(__file__).resolve().parent
 
 SMALL_DIMS = [(1, 1, 1), (5, 3, 40), (47, 2, 33), (8, 8, 64), (32, 8, 512), (64, 64, 512)]
 SEEDS = [1, 42, 7]
+SWEEP_NGPOWN = (16, 33, 66, 132, 264, 528)
+SWEEP_NCOULS = (8192, 16384, 32768, 65536)
 
 
 @contextmanager
@@ -100,9 +105,22 @@ def make_case(dims, seed, nw, with_reference: bool, versions: bool = True) -> di
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
-    ap.add_argument("--append", choices=("weak-nw3",),
+    ap.add_argument("--append", choices=("weak-nw3", "sweep"),
                     help="append one big case to the existing gpp_big.json and stop")
     args = ap.parse_args()
+
+    if args.append == "sweep":
+        path = HERE / "gpp_big.json"
+        big = json.loads(path.read_text())
+        have = {(tuple(c["dims"]), c["seed"], c["nw"]) for c in big["cases"]}
+        for ngpown in SWEEP_NGPOWN:
+            for ncouls in SWEEP_NCOULS:
+                key = ((512, ngpown, ncouls), 1, 3)
+                if key in have:
+                    continue
+                big["cases"].append(make_case(key[0], 1, 3, with_reference=False, versions=False))
+                path.write_text(json.dumps(big, indent=1) + "\n")  # checkpoint per point
+        return
 
     if args.append == "weak-nw3":
         # The bench's weak workload at its default frequency count (nw 3).

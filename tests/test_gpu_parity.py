@@ -58,15 +58,43 @@ def test_small_cases_vs_reference(case, variant):
 
 @pytest.mark.parametrize("case", BIG, ids=_ids(BIG))
 def test_big_cases_vs_reference(case):
+    """Paper, weak and all 24 aspect-ratio sweep points (BASELINE configs[1],
+    [3], [4]) against the unmodified reference's outputs.  The inputs are
+    drawn on the device (gpp_synth, bit-exact with synth_problem:
+    test_device_synthesis_is_bitexact); both kernels run -- the counting one
+    for the exact near/far counts and the production one evaluate_variant
+    uses."""
     nb, ng, nc = case["dims"]
-    p = synth_problem(nb, ng, nc, seed=case["seed"], nw=case["nw"], check=nb * ng * nc < 10**10)
-    got, stats, _ = evaluate(p, "rcp_sq")
-    fast = evaluate_variant(p, "rcp_sq")
+    ctx = GPPContext(0)
+    try:
+        ctx.synth(nb, ng, nc, seed=case["seed"], nw=case["nw"])
+        got, (near, far), _ = ctx.run("rcp_sq", counts=True)
+        fast = ctx.run("rcp_sq", counts=False)[0]
+    finally:
+        ctx.close()
     want = _R(case.get("reference_result") or case["evaluate_variant"]["rcp_sq"])
     for r in (got, fast):
         err = max_rel_error(r, want)
         assert err <= TOL, err
-    assert [stats.instances, stats.near, stats.far] == case["branch_stats"]["rcp_sq"]
+    assert [case["nw"] * nb * ng * nc, near, far] == case["branch_stats"]["rcp_sq"]
+
+
+def test_paper_size_public_path_vs_reference():
+    """evaluate_variant on host arrays (first call: upload pipelined with the
+    kernel; second: resident) at the paper size, nw 2 and 3."""
+    for nw in (2, 3):
+        case = next(c for c in BIG if c["dims"] == [512, 66, 32768] and c["seed"] == 1 and c["nw"] == nw)
+        p = synth_problem(512, 66, 32768, seed=1, nw=nw, check=False)
+        first = evaluate_variant(p, "rcp_sq")
+        again = evaluate_variant(p, "rcp_sq")
+        assert _bits_equal(first, again)
+        want = _R(case.get("reference_result") or case["evaluate_variant"]["rcp_sq"])
+        assert max_rel_error(first, want) <= TOL
+        assert [branch_stats(p, "rcp_sq").near, branch_stats(p, "rcp_sq").far] == case["branch_stats"]["rcp_sq"][1:]
+
+
+def _bits_equal(a, b) -> bool:
+    return np.array_equal(a.achtemp, b.achtemp) and np.array_equal(a.asxtemp, b.asxtemp)
 
 
 def test_plain_variants_paper_size():
@@ -137,23 +165,43 @@ def _run(p, band_range):
         ctx.close()
 
 
-def test_deterministic_bitwise():
-    """Static item schedules: the same path gives the same bits.  (The
-    pipelined first call sums per ig slab, a different -- equally fixed --
-    order than the resident single launch.)"""
-    p = synth_problem(128, 66, 4096, seed=1, nw=3)
-    first = evaluate_variant(p, "rcp_sq")          # pipelined upload + evaluate
-    a = evaluate_variant(p, "rcp_sq")              # resident
-    b = evaluate_variant(p, "rcp_sq")
-    assert np.array_equal(a.achtemp, b.achtemp) and np.array_equal(a.asxtemp, b.asxtemp)
-    assert max_rel_error(first, a) <= 1e-13
-    ctx = GPPContext(0)
-    try:
-        c = ctx.evaluate_host(p, "rcp_sq")[0]
-        d = ctx.evaluate_host(p, "rcp_sq")[0]
-        assert np.array_equal(c.achtemp, d.achtemp) and np.array_equal(c.asxtemp, d.asxtemp)
-    finally:
-        ctx.close()
+@pytest.mark.parametrize("dims,nw", [((128, 66, 4096), 3), ((512, 66, 32768), 3),
+                                     ((600, 33, 5000), 2), ((1100, 17, 9000), 3),
+                                     ((300, 10, 3000), 1), ((64, 9, 700), 5)])
+def test_bitwise_reproducible_on_every_path(dims, nw):
+    """fixed inputs and variant give the same bits whatever
+    the path: the first call (upload pipelined with the kernel over ig slabs),
+    the resident re-run, any slab count, a fresh context.  Every schedule runs
+    the same canonical items and the finalize sums them in slot order."""
+    p = synth_problem(*dims, seed=1, nw=nw, check=False)
+    for variant in ("rcp_sq", "div"):
+        if variant == "div" and dims[0] * dims[1] * dims[2] > 10**8:
+            continue
+        first = evaluate_variant(p, variant)          # pipelined upload + evaluate
+        again = evaluate_variant(p, variant)          # resident
+        assert _bits_equal(first, again), variant
+        ctx = GPPContext(0)
+        try:
+            for slabs in (1, 2, 3, 7, 0):
+                r = ctx.evaluate_host(p, variant, slabs=slabs)[0]
+                assert _bits_equal(r, first), (variant, slabs)
+            ctx.upload(p, force=True)
+            assert _bits_equal(ctx.run(variant, counts=False)[0], first), variant
+        finally:
+            ctx.close()
+
+
+def test_versions_sharing_a_variant_agree_bitwise():
+    """rooflab test_gpp.py:88-94 on this package: run_version's result comes
+    from the version's variant alone (runner.py:258-260)."""
+    for dims in ((64, 64, 512), (512, 66, 32768)):
+        p = synth_problem(*dims, seed=1, nw=3, check=False)
+        by_name = {name: run_version(p, name).result for name in
+                   ("v0", "v1", "v2", "v3", "v4", "v5", "v6", "v7", "v8")}
+        assert _bits_equal(by_name["v1"], by_name["v2"])
+        for name in ("v4", "v5", "v6", "v7", "v8"):
+            assert _bits_equal(by_name["v3"], by_name[name]), name
+        assert _bits_equal(by_name["v8"], evaluate_variant(p, "rcp_sq"))
 
 
 def test_writeable_inputs_are_reuploaded():
@@ -451,3 +499,70 @@ def test_concurrent_contexts_from_threads():
         t.join()
     assert errs[0] is not None and errs[1] is not None
     assert max(errs) <= TOL
+
+
+def test_public_seam_is_thread_safe():
+    """The drop-in path itself (evaluate_variant / branch_stats, no explicit
+    context) called from four threads at once with different problems and
+    variants: every call returns exactly the bits of the same call made
+    alone (per-thread contexts)."""
+    import threading
+
+    probs = [synth_problem(200, 7, 5000, seed=s, nw=nw, check=False)
+             for s, nw in ((3, 3), (4, 2), (5, 3), (6, 1))]
+    variants = ["rcp_sq", "rcp_sq", "rcp", "rcp_sq"]
+    alone = [evaluate_variant(p, v) for p, v in zip(probs, variants)]
+    counts = [branch_stats(p, "rcp_sq") for p in probs]
+    bad = []
+    barrier = threading.Barrier(4)
+
+    def work(k):
+        barrier.wait()
+        for i in range(8):
+            # alternate fresh (writeable copy: pipelined upload) and resident calls
+            q = probs[k]
+            if i % 2:
+                q = GPPProblem(q.nbands, q.ngpown, q.ncouls, q.wtilde.copy(order="F"),
+                               q.i_eps.copy(order="F"), q.aqsntemp.copy(order="F"),
+                               q.aqsmtemp.copy(order="F"), q.wx.copy())
+            got = evaluate_variant(q, variants[k])
+            if not _bits_equal(got, alone[k]):
+                bad.append((k, i))
+            s = branch_stats(q, "rcp_sq")
+            if (s.near, s.far) != (counts[k].near, counts[k].far):
+                bad.append((k, i, "counts"))
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert bad == []
+
+
+def test_shared_context_serialises_callers():
+    """One explicit GPPContext driven from two threads: the library's
+    per-context lock serialises the calls, so each thread's result is its own
+    problem's, bit for bit."""
+    import threading
+
+    probs = [synth_problem(100, 5, 3000, seed=s, nw=3, check=False) for s in (8, 9)]
+    alone = [evaluate_variant(p, "rcp_sq") for p in probs]
+    ctx = GPPContext(0)
+    bad = []
+
+    def work(k):
+        for _ in range(10):
+            got = ctx.evaluate_host(probs[k], "rcp_sq")[0]
+            if not _bits_equal(got, alone[k]):
+                bad.append(k)
+
+    try:
+        ts = [threading.Thread(target=work, args=(k,)) for k in range(2)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    finally:
+        ctx.close()
+    assert bad == []
