@@ -689,7 +689,6 @@ struct SaccSmem {
 
 struct SaccItem {
   int igpt, igb, b0, nb;
-  int row, chunk;
 };
 
 __device__ __forceinline__ SaccItem sacc_item(const Params& p, unsigned item) {
@@ -697,13 +696,18 @@ __device__ __forceinline__ SaccItem sacc_item(const Params& p, unsigned item) {
   const unsigned bcu = fastdiv(item, p.rows_mul, p.rows_shift);
   const unsigned row = item - bcu * static_cast<unsigned>(p.n_rows) + static_cast<unsigned>(p.row0);
   const unsigned igb = fastdiv(row, p.igpt_mul, p.igpt_shift);
-  it.row = static_cast<int>(row);
-  it.chunk = static_cast<int>(bcu);
   it.igpt = static_cast<int>(row - igb * p.n_igptile);
   it.igb = static_cast<int>(igb);
   it.b0 = static_cast<int>(bcu) * p.bchunk;
   it.nb = min(p.bchunk, p.nbands - it.b0);
   return it;
+}
+
+// The canonical slot of an item (Params::slot_base).
+__device__ __forceinline__ long long sacc_slot(const Params& p, unsigned item) {
+  const unsigned bcu = fastdiv(item, p.rows_mul, p.rows_shift);
+  const unsigned row = item - bcu * static_cast<unsigned>(p.n_rows) + static_cast<unsigned>(p.row0);
+  return p.slot_base + static_cast<long long>(bcu) * p.slot_stride + row;
 }
 
 // This thread's ig for an item (clamped to a valid column for padded lanes).
@@ -932,7 +936,6 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
   extern __shared__ __align__(16) unsigned char sacc_smem_raw[];
   SaccSmem<NW, IGP_T>& sm = *reinterpret_cast<SaccSmem<NW, IGP_T>*>(sacc_smem_raw);
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
   Acc<1> cnt;
   cnt.nn = 0;
   cnt.nf = 0;
@@ -1052,11 +1055,20 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
     for (int off = 16; off > 0; off >>= 1)
 #pragma unroll
       for (int k = 0; k < 4 * NW; ++k) a[k] += __shfl_xor_sync(0xffffffffu, a[k], off);
-    if (lane == 0) {
-      const long long slot = p.slot_base + static_cast<long long>(it.chunk) * p.slot_stride + it.row;
-      double2* dst = reinterpret_cast<double2*>(p.partials + (slot * (kThreads / 32) + warp) * (4 * NW));
+    // Lane 0 stores the row with predicated stores (no branch: a divergent
+    // region inside the item loop costs the band loop its uniform-datapath
+    // wx indexing).
+    {
+      unsigned tid_l;  // read afresh: not held across the band loop
+      asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid_l));
+      const unsigned leader = (tid_l & 31) == 0;
+      double2* dst = reinterpret_cast<double2*>(
+          p.partials + (sacc_slot(p, item) * (kThreads / 32) + (tid_l >> 5)) * (4 * NW));
 #pragma unroll
-      for (int k = 0; k < 2 * NW; ++k) dst[k] = make_double2(a[2 * k], a[2 * k + 1]);
+      for (int k = 0; k < 2 * NW; ++k)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
+                     "@p st.global.v2.f64 [%1], {%2, %3};\n\t}"
+                     ::"r"(leader), "l"(dst + k), "d"(a[2 * k]), "d"(a[2 * k + 1]) : "memory");
     }
 
     if (!has_next) break;
@@ -1071,6 +1083,7 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_cons
   cp_async_wait<0>();
 
   if constexpr (COUNT) {
+    const int lane = tid & 31, warp = tid >> 5;
     __syncthreads();
     // The aqsntemp ring is idle now: reuse it for the per-warp counts.
     unsigned long long* s_cnt = reinterpret_cast<unsigned long long*>(&sm.an[0][0]);

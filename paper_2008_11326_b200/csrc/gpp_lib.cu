@@ -621,7 +621,7 @@ struct EvalRun {
   bool count = false, sacc = false;
   std::vector<std::pair<int, int>> groups;
   std::vector<const Canon*> canon;   // per group (production kernel)
-  std::vector<long long> slot_off;   // per group: first slot in c->partials
+  std::vector<size_t> part_off;      // per group: first double of its slots in c->partials
   cudaEvent_t* ev_main = nullptr;
   int piece = 0;
   std::vector<cudaEvent_t> pending;  // other kernels: waits deferred to eval_end
@@ -636,7 +636,7 @@ int eval_begin(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, EvalRu
   nw_groups(c->nw, max_group(variant), &r->groups);
   r->sacc = variant == GPP_VARIANT_RCP_SQ;
   if (r->sacc) {
-    long long off = 0, max_slots = 0;
+    long long max_slots = 0;
     size_t doubles = 0;
     for (const auto& g : r->groups) {
       const Canon* cn = nullptr;
@@ -644,8 +644,7 @@ int eval_begin(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, EvalRu
       if (rc) return rc;
       if (cn->n_slots >= (1ll << 31)) return fail(GPP_ERR_ARG, "too many work items");
       r->canon.push_back(cn);
-      r->slot_off.push_back(off);
-      off += cn->n_slots;
+      r->part_off.push_back(doubles);
       max_slots = std::max(max_slots, cn->n_slots);
       doubles += static_cast<size_t>(cn->n_slots) * (gpp::kThreads / 32) * 4 * g.second;
     }
@@ -697,9 +696,9 @@ int launch_sacc(gpp_ctx* c, const EvalRun& r, size_t gi, const SaccLaunch& L, co
   p.bchunk = L.bchunk;
   p.n_items = L.n_items;
   p.wxmax = c->wxmax;
-  p.slot_base = r.slot_off[gi] + C.slot0 - C.row0;
+  p.slot_base = C.slot0 - C.row0;
   p.slot_stride = C.n_rows;
-  p.partials = c->partials.ptr;
+  p.partials = c->partials.ptr + r.part_off[gi];
   p.cpartials = c->cpartials.ptr + 2 * gi;
   const long long slots = static_cast<long long>(cn.pl.blocks_per_sm) * c->num_sms;
   const int grid = static_cast<int>(std::min<long long>(slots, p.n_items));
@@ -812,9 +811,7 @@ int eval_end(gpp_ctx* c, EvalRun* r) {
     const int iw0 = r->groups[gi].first, nwg = r->groups[gi].second;
     const long long n_slots = r->canon[gi]->n_slots;
     const int grid = static_cast<int>((n_slots + kSlotsPerFinalizeBlock - 1) / kSlotsPerFinalizeBlock);
-    const double* part = c->partials.ptr;
-    for (size_t k = 0; k < gi; ++k)
-      part += static_cast<size_t>(r->canon[k]->n_slots) * (gpp::kThreads / 32) * 4 * r->groups[k].second;
+    const double* part = c->partials.ptr + r->part_off[gi];
     pick_slot_finalize(nwg)<<<grid, 256, 0, c->stream>>>(
         part, n_slots, kSlotsPerFinalizeBlock, c->stage.ptr, c->ticket.ptr,
         c->cpartials.ptr + 2 * gi, 1, c->nw, iw0, gi == 0 ? 1 : 0, r->count ? 1 : 0, c->out.ptr,
@@ -1079,16 +1076,17 @@ std::vector<int> slab_schedule(gpp_ctx* c, const EvalRun& r, int n_blk, int slab
                                     cn.pl.n_igptile;
       tail_blocks = std::max(0, tail_blocks / cn.pl.n_igptile);
     }
+    // Built from the end: the tail blocks, then slabs growing by ~1.25x up to
+    // two waves of rows (tools/probe_slabs3.py: 6.57 ms end to end at the
+    // paper size against 6.72-7.0 ms for equal slabs of 4-16 blocks).
     std::vector<int> rev;
-    int sum = 0;
-    if (tail_blocks > 0 && tail_blocks < n_blk) {
-      rev.push_back(tail_blocks);
-      sum = tail_blocks;
-    }
+    int sum = 0, sz = std::max(1, tail_blocks);
+    if (tail_blocks <= 0 || tail_blocks >= n_blk) sz = 1;
     while (sum < n_blk) {
-      const int sz = std::min(per, n_blk - sum);
-      rev.push_back(sz);
-      sum += sz;
+      const int take = std::min(sz, n_blk - sum);
+      rev.push_back(take);
+      sum += take;
+      sz = std::min(2 * per, std::max(sz + 1, static_cast<int>(std::ceil(sz * 1.25))));
     }
     sizes.assign(rev.rbegin(), rev.rend());
   }
