@@ -4,6 +4,7 @@
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <omp.h>
 
 #include <algorithm>
 #include <cmath>
@@ -147,6 +148,15 @@ struct gpp_ctx {
   size_t h_out_cap = 0;
   double* h_wx = nullptr;              // pinned staging for the expanded wx
   size_t h_wx_cap = 0;
+
+  // Pinned staging ring for pageable host inputs (copy_rows): kStageSlots
+  // buffers of stage_cap bytes; slot k is free once stage_ev[k] completed.
+  static constexpr int kStageSlots = 4;
+  unsigned char* h_stage[kStageSlots] = {nullptr, nullptr, nullptr, nullptr};
+  size_t stage_cap = 0;
+  cudaEvent_t stage_ev[kStageSlots] = {nullptr, nullptr, nullptr, nullptr};
+  int stage_next = 0;
+  uint64_t staged_bytes = 0;  // bytes that went through the staging ring (gpp_stats)
 
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
@@ -904,6 +914,10 @@ void gpp_destroy(gpp_ctx* c) {
     if (c->h_out) cudaFreeHost(c->h_out);
     if (c->h_counts) cudaFreeHost(c->h_counts);
     if (c->h_wx) cudaFreeHost(c->h_wx);
+    for (int k = 0; k < gpp_ctx::kStageSlots; ++k) {
+      if (c->h_stage[k]) cudaFreeHost(c->h_stage[k]);
+      if (c->stage_ev[k]) cudaEventDestroy(c->stage_ev[k]);
+    }
     for (auto& ev : c->ev)
       if (ev) cudaEventDestroy(ev);
     for (auto& ev : c->slab_ev) cudaEventDestroy(ev);
@@ -1017,20 +1031,121 @@ int copy_small(gpp_ctx* c, const HostProblem& h, cudaStream_t s) {
   return copy_small_wx(c, h, s);
 }
 
-// H2D of the ig rows [i0, i1) of wtilde, i_eps and the aqsntemp shard:
-// strided (2D) copies of the F-order arrays, one row segment per column.
-int copy_rows(gpp_ctx* c, const HostProblem& h, int64_t i0, int64_t i1, cudaStream_t s) {
-  const size_t pitch = static_cast<size_t>(h.ncouls) * sizeof(double2);
-  const size_t width = static_cast<size_t>(i1 - i0) * sizeof(double2);
-  const size_t off = static_cast<size_t>(i0);
-  GPP_CUDA(cudaMemcpy2DAsync(c->wtilde.ptr + off, pitch, h.wtilde + 2 * off, pitch, width,
-                             h.ngpown, cudaMemcpyHostToDevice, s));
-  GPP_CUDA(cudaMemcpy2DAsync(c->eps.ptr + off, pitch, h.i_eps + 2 * off, pitch, width, h.ngpown,
-                             cudaMemcpyHostToDevice, s));
-  GPP_CUDA(cudaMemcpy2DAsync(c->aqsn.ptr + off, pitch,
-                             h.aqsntemp + 2 * (static_cast<size_t>(h.band0) * h.ncouls + off),
-                             pitch, width, h.band1 - h.band0, cudaMemcpyHostToDevice, s));
+// Whether a host range is page-locked (cudaHostRegister / cudaMallocHost):
+// the DMA engines then read it directly.
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Host threads that pack pageable inputs into the staging ring:
+// GPP_HOST_THREADS, else the cores this process's share of the node
+// (LOCAL_WORLD_SIZE ranks per node under torchrun), at most 16.
+int host_threads() {
+  static const int n = [] {
+    if (const char* e = std::getenv("GPP_HOST_THREADS")) return std::max(1, std::atoi(e));
+    int local = 1;
+    if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) local = std::max(1, std::atoi(e));
+    const int hw = std::max(1, omp_get_num_procs());
+    return std::max(1, std::min(16, hw / local));
+  }();
+  return n;
+}
+
+// One staging buffer: 8 MB (GPP_STAGE_MB overrides, for experiments).
+size_t stage_bytes() {
+  static const size_t n = [] {
+    const char* e = std::getenv("GPP_STAGE_MB");
+    const long mb = e ? std::max(1L, std::atol(e)) : 8L;
+    return static_cast<size_t>(mb) << 20;
+  }();
+  return n;
+}
+
+int ensure_stage(gpp_ctx* c) {
+  if (c->stage_cap >= stage_bytes()) return GPP_OK;
+  for (int k = 0; k < gpp_ctx::kStageSlots; ++k) {
+    if (c->h_stage[k]) {
+      if (c->stage_ev[k]) GPP_CUDA(cudaEventSynchronize(c->stage_ev[k]));
+      cudaFreeHost(c->h_stage[k]);
+      c->h_stage[k] = nullptr;
+    }
+    GPP_CUDA(cudaMallocHost(&c->h_stage[k], stage_bytes()));
+    if (!c->stage_ev[k]) GPP_CUDA(cudaEventCreateWithFlags(&c->stage_ev[k], cudaEventDisableTiming));
+  }
+  c->stage_cap = stage_bytes();
   return GPP_OK;
+}
+
+// H2D of rows [i0, i1) of `ncol` columns (column pitch `ld` elements) of a
+// complex F-order host array into the device array of the same layout.
+// Pinned source: one strided copy.  Pageable source: columns are packed by
+// host_threads() threads into the next pinned staging buffer (waiting until
+// its previous copy has drained) and copied from there, buffer by buffer, so
+// the packing of one buffer overlaps the DMA of the previous ones.
+int copy_cols(gpp_ctx* c, double2* dst, const double* src, int64_t ld, int64_t ncol, int64_t i0,
+              int64_t i1, bool pinned, cudaStream_t s) {
+  const size_t pitch = static_cast<size_t>(ld) * sizeof(double2);
+  const size_t width = static_cast<size_t>(i1 - i0) * sizeof(double2);
+  if (ncol <= 0 || width == 0) return GPP_OK;
+  if (pinned) {
+    GPP_CUDA(cudaMemcpy2DAsync(dst + i0, pitch, src + 2 * i0, pitch, width, ncol,
+                               cudaMemcpyHostToDevice, s));
+    return GPP_OK;
+  }
+  int rc = ensure_stage(c);
+  if (rc) return rc;
+  const int64_t per = std::max<int64_t>(1, static_cast<int64_t>(c->stage_cap / width));
+  const int nt = host_threads();
+  for (int64_t c0 = 0; c0 < ncol; c0 += per) {
+    const int64_t c1 = std::min(ncol, c0 + per);
+    const int k = c->stage_next;
+    c->stage_next = (k + 1) % gpp_ctx::kStageSlots;
+    GPP_CUDA(cudaEventSynchronize(c->stage_ev[k]));  // its previous copy has drained
+    unsigned char* buf = c->h_stage[k];
+    const size_t wbytes = width;
+    const int64_t ncols = c1 - c0;
+    if (ncols * static_cast<int64_t>(wbytes) >= (int64_t{1} << 20) && nt > 1) {
+#pragma omp parallel for num_threads(nt) schedule(static)
+      for (int64_t j = 0; j < ncols; ++j)
+        std::memcpy(buf + j * wbytes, src + 2 * ((c0 + j) * ld + i0), wbytes);
+    } else {
+      for (int64_t j = 0; j < ncols; ++j)
+        std::memcpy(buf + j * wbytes, src + 2 * ((c0 + j) * ld + i0), wbytes);
+    }
+    GPP_CUDA(cudaMemcpy2DAsync(dst + c0 * ld + i0, pitch, buf, wbytes, wbytes, ncols,
+                               cudaMemcpyHostToDevice, s));
+    GPP_CUDA(cudaEventRecord(c->stage_ev[k], s));
+    c->staged_bytes += static_cast<uint64_t>(ncols) * wbytes;
+  }
+  return GPP_OK;
+}
+
+// Pinned-ness of the three row-copied inputs (checked once per call).
+struct HostPins {
+  bool wtilde = false, eps = false, aqsn = false;
+};
+HostPins host_pins(const HostProblem& h) {
+  HostPins p;
+  p.wtilde = host_pinned(h.wtilde);
+  p.eps = host_pinned(h.i_eps);
+  p.aqsn = host_pinned(h.aqsntemp);
+  return p;
+}
+
+// H2D of the ig rows [i0, i1) of wtilde, i_eps and the aqsntemp shard.
+int copy_rows(gpp_ctx* c, const HostProblem& h, const HostPins& pins, int64_t i0, int64_t i1,
+              cudaStream_t s) {
+  int rc = copy_cols(c, c->wtilde.ptr, h.wtilde, h.ncouls, h.ngpown, i0, i1, pins.wtilde, s);
+  if (!rc) rc = copy_cols(c, c->eps.ptr, h.i_eps, h.ncouls, h.ngpown, i0, i1, pins.eps, s);
+  if (!rc)
+    rc = copy_cols(c, c->aqsn.ptr, h.aqsntemp + 2 * static_cast<size_t>(h.band0) * h.ncouls,
+                   h.ncouls, h.band1 - h.band0, i0, i1, pins.aqsn, s);
+  return rc;
 }
 
 // ig-slab schedule of the pipelined evaluate, as block offsets.  The copy is
@@ -1043,7 +1158,7 @@ int copy_rows(gpp_ctx* c, const HostProblem& h, int64_t i0, int64_t i1, cudaStre
 // balanced-tail rows (short items: little work after the last byte).
 // slabs > 0: that many equal slabs.  GPP_SLABS="b0,b1,..." (block counts
 // summing to the block total) overrides, for experiments.
-std::vector<int> slab_schedule(gpp_ctx* c, const EvalRun& r, int n_blk, int slabs) {
+std::vector<int> slab_schedule(gpp_ctx* c, const EvalRun& r, int n_blk, int slabs, bool pageable) {
   std::vector<int> sizes;
   if (const char* e = std::getenv("GPP_SLABS")) {
     int sum = 0;
@@ -1076,17 +1191,25 @@ std::vector<int> slab_schedule(gpp_ctx* c, const EvalRun& r, int n_blk, int slab
                                     cn.pl.n_igptile;
       tail_blocks = std::max(0, tail_blocks / cn.pl.n_igptile);
     }
-    // Built from the end: the tail blocks, then slabs growing by ~1.25x up to
-    // two waves of rows (tools/probe_slabs3.py: 6.57 ms end to end at the
-    // paper size against 6.72-7.0 ms for equal slabs of 4-16 blocks).
+    // Built from the end: the tail blocks, then growing slabs.  Pinned
+    // inputs: by ~1.25x up to two waves of rows (tools/probe_slabs3.py: 6.57
+    // ms end to end at the paper size against 6.72-7.0 ms for equal slabs of
+    // 4-16 blocks).  Pageable inputs (packed into the staging ring, where
+    // narrow slabs pack slowly): doubling up to one wave, then +1 wave up to
+    // five (tools/probe_pageable3.py: 7.0-7.2 ms against 7.5 for the taper).
     std::vector<int> rev;
     int sum = 0, sz = std::max(1, tail_blocks);
     if (tail_blocks <= 0 || tail_blocks >= n_blk) sz = 1;
+    bool first = true;
     while (sum < n_blk) {
       const int take = std::min(sz, n_blk - sum);
       rev.push_back(take);
       sum += take;
-      sz = std::min(2 * per, std::max(sz + 1, static_cast<int>(std::ceil(sz * 1.25))));
+      if (pageable)
+        sz = first ? sz : std::min(5 * per, sz < per ? 2 * sz : sz + per);
+      else
+        sz = std::min(2 * per, std::max(sz + 1, static_cast<int>(std::ceil(sz * 1.25))));
+      first = false;
     }
     sizes.assign(rev.rbegin(), rev.rend());
   }
@@ -1135,7 +1258,7 @@ int gpp_upload(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32
   cudaStream_t s = c->stream;
   rc = copy_small(c, h, s);
   if (rc) return rc;
-  rc = copy_rows(c, h, 0, ncouls, s);
+  rc = copy_rows(c, h, host_pins(h), 0, ncouls, s);
   if (rc) return rc;
   GPP_CUDA(cudaStreamSynchronize(s));
   c->have_problem = true;
@@ -1168,7 +1291,9 @@ int gpp_evaluate_host(gpp_ctx* c, int32_t variant, int64_t nbands, int64_t ngpow
   EvalRun r;
   rc = eval_begin(c, variant, near_far != nullptr, nullptr, &r);
   if (rc) return rc;
-  const std::vector<int> blk0 = slab_schedule(c, r, n_blk, slabs);
+  const HostPins pins = host_pins(h);
+  const std::vector<int> blk0 =
+      slab_schedule(c, r, n_blk, slabs, !(pins.wtilde && pins.eps && pins.aqsn));
   const int n_sched = static_cast<int>(blk0.size()) - 1;
   while (static_cast<int>(c->slab_ev.size()) < n_sched + 1) {
     cudaEvent_t e;
@@ -1181,7 +1306,7 @@ int gpp_evaluate_host(gpp_ctx* c, int32_t variant, int64_t nbands, int64_t ngpow
   for (int sl = 0; sl < n_sched; ++sl) {
     const int64_t i0 = static_cast<int64_t>(blk0[sl]) * gpp::kThreads;
     const int64_t i1 = std::min<int64_t>(ncouls, static_cast<int64_t>(blk0[sl + 1]) * gpp::kThreads);
-    rc = copy_rows(c, h, i0, i1, c->cstream);
+    rc = copy_rows(c, h, pins, i0, i1, c->cstream);
     if (rc) return rc;
     GPP_CUDA(cudaEventRecord(c->slab_ev[sl], c->cstream));
     rc = eval_rows(c, &r, blk0[sl], blk0[sl + 1], c->slab_ev[sl]);
