@@ -7,24 +7,41 @@
 Workload (BASELINE.json configs[1]): the paper size (nbands, ngpown, ncouls) =
 (512, 66, 32768) with 3 frequencies, synth_problem seed 1 (3.5 % far-branch
 instances; seed 42 never takes the far branch).  At N GPUs the
-band (n1) loop is sharded across ranks (strong scaling, BASELINE configs[2]);
-the per-rank partial achtemp/asxtemp and branch counts are combined by one
-NCCL allreduce inside the library.
+band (n1) loop is sharded (strong scaling, BASELINE configs[2]) and the
+partials are combined by one NCCL allreduce inside the library -- one
+process per GPU under torchrun, or, without torchrun, one process driving N
+devices (gpp_comm_init_all + gpp_time_group).
 
-A step = one full evaluation of the reduction (main kernel + deterministic
-finalize (+ allreduce)).  `value` = algorithmic FP64 FLOPs of the whole job
-(the reference's analytic count, rooflab/gpp/kernel.py:191-212 with the
-kernel's exact near/far counts) / device time (CUDA events, max over ranks).
-`e2e` = the same metric through the public API with pinned host inputs:
-H2D of every input, the evaluation and the D2H of the result each step.
+A step = one full evaluation of the reduction (production kernel + slot
+finalize (+ allreduce)), inputs resident in HBM (338 MB > the 126 MB L2, so
+every step streams them from HBM; no flush needed).
+
+Metric (BASELINE.json): "GPP FP64 TFLOP/s (ncu-counted)".  `value` = FP64
+FLOPs the kernels EXECUTE per step (2*dfma + dmul + dadd, ncu's
+smsp__sass_thread_inst_executed_op_{dfma,dmul,dadd}_pred_on.sum -- the
+reference's profiler column names, rooflab/metrics.py:228-237), counted by
+a live ncu capture of this build in a child process after the timed region,
+summed over all GPUs' shards, / device time (CUDA events, max over ranks).
+The reference's analytic count (rooflab/gpp/kernel.py:191-212) / the same
+time is `effective_tflops` beside it: the kernel executes ~65 % of those
+FLOPs (per-instance algebra), so that rate is not a roofline
+figure.  `e2e` = the same numerator per step through the
+public API (evaluate_variant on pageable numpy arrays: H2D of every input,
+the evaluation and the D2H of the result).  The reference arm uses the same
+numerator, so the driver's ratio of the two lines is a pure time ratio.
 """
 
 from __future__ import annotations
 
 import argparse
+import csv
+import hashlib
+import io
 import json
 import os
+import platform
 import statistics
+import struct
 import subprocess
 import sys
 import threading
@@ -42,6 +59,17 @@ WORKLOADS = {
     "tiny": (32, 8, 512),
     "weak": (4096, 528, 65536),
 }
+LIB = ROOT / "paper_2008_11326_b200" / "lib" / "libgpp_b200.so"
+NCU_SUMMARY = ROOT / "profiles" / "ncu_summary.json"
+NCU_METRICS = (
+    "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
+    "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
+    "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
+    "dram__bytes_read.sum",
+    "dram__bytes_write.sum",
+    "gpu__time_duration.sum",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+)
 
 
 def parse_args():
@@ -59,22 +87,48 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the live ncu capture")
+    ap.add_argument("--ncu-child", action="store_true", help=argparse.SUPPRESS)
     a = ap.parse_args()
     if a.seed is None:
         a.seed = 42 if a.workload == "weak" else 1
     return a
 
 
+def lib_sha256() -> str | None:
+    """sha256 of the library's device code (its .nv_fatbin ELF section: the
+    sm_100a kernels ncu counts).  nvcc rebuilds it bit for bit from the same
+    sources, unlike the host part of the .so."""
+    try:
+        b = LIB.read_bytes()
+        shoff, = struct.unpack_from("<Q", b, 0x28)
+        shentsize, shnum, shstrndx = struct.unpack_from("<HHH", b, 0x3A)
+        secs = [struct.unpack_from("<IIQQQQIIQQ", b, shoff + i * shentsize) for i in range(shnum)]
+        stro = secs[shstrndx][4]
+        for sec in secs:
+            name = b[stro + sec[0]: b.index(b"\0", stro + sec[0])]
+            if name == b".nv_fatbin":
+                return "fatbin:" + hashlib.sha256(b[sec[4]: sec[4] + sec[5]]).hexdigest()
+        return None
+    except (OSError, struct.error, ValueError, IndexError):
+        return None
+
+
 # ----------------------------------------------------------------------------
 # distributed plumbing
 # ----------------------------------------------------------------------------
 class Dist:
+    """torchrun (WORLD_SIZE set): one process per GPU over NCCL.  Otherwise
+    one process; --gpus N > 1 then drives N local devices itself."""
+
     def __init__(self, gpus: int):
+        self.torchrun = "WORLD_SIZE" in os.environ
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-        if self.world != gpus:
-            raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={self.world}; launch with torchrun for N>1")
+        if self.torchrun and self.world != gpus:
+            raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={self.world}")
+        self.gpus = gpus
         self.pg = None
         if self.world > 1:
             import torch
@@ -84,14 +138,13 @@ class Dist:
             dist.init_process_group("nccl", device_id=torch.device("cuda", self.local_rank))
             self.pg = dist
 
+    @property
+    def single_process_group(self) -> bool:
+        return not self.torchrun and self.gpus > 1
+
     def barrier(self):
         if self.pg:
             self.pg.barrier()
-
-    def sync(self):
-        import torch
-
-        torch.cuda.synchronize()
 
     def max(self, x: float) -> float:
         if not self.pg:
@@ -102,131 +155,257 @@ class Dist:
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
 
+    def sum(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t)
+        return float(t.item())
+
     def close(self):
         if self.pg:
             self.pg.destroy_process_group()
 
 
 # ----------------------------------------------------------------------------
-# clocks sampler (nvidia-smi during the timed region)
+# clocks sampler: NVML every 5 ms during the timed region (nvidia-smi fallback)
 # ----------------------------------------------------------------------------
 class Clocks:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, devices):
-        self.devices = devices
+        self.devices = list(devices)
         self.rows = []
-        self.proc = None
+        self.stop_ev = threading.Event()
+        self.thread = None
+        self.err = None
 
     def start(self):
+        if not self.devices:
+            return
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
-                 "-i", ",".join(str(d) for d in self.devices)],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except OSError:
-            self.proc = None
+            import pynvml
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 8:
-                self.rows.append(parts)
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handles = [pynvml.nvmlDeviceGetHandleByIndex(d) for d in self.devices]
+        except Exception as e:  # noqa: BLE001
+            self.err = f"nvml unavailable: {e}"
+            return
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
 
-    def stop(self) -> dict:
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.15)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
+    def _run(self):
+        nv = self.nvml
+        while not self.stop_ev.is_set():
+            for h in self.handles:
+                try:
+                    self.rows.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                      nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM),
+                                      nv.nvmlDeviceGetPowerUsage(h) / 1000.0,
+                                      nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                except Exception:  # noqa: BLE001
+                    pass
+            time.sleep(0.005)
+
+    def stop(self) -> dict | None:
+        if not self.devices:
+            return None
+        if self.thread is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "no samples"]}
+        self.stop_ev.set()
         self.thread.join(timeout=2)
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        pw = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i] == "Active"})
-        return {
-            "sm_mhz": statistics.median(sm) if sm else None,
-            "sm_max_mhz": max(mx) if mx else None,
-            "power_w_max": max(pw) if pw else None,
-            "samples": len(self.rows),
-            "reasons": reasons,
-        }
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({k for r in self.rows for k, bit in self.REASONS.items() if r[3] & bit})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(r[1] for r in self.rows) if self.rows else None,
+                "power_w_max": max(r[2] for r in self.rows) if self.rows else None,
+                "samples": len(self.rows), "sampler": "nvml 5 ms", "reasons": reasons}
 
 
 # ----------------------------------------------------------------------------
-# CPU baseline (reference CPU path, restated in oracle/): rank 0 only
+# host description (cpu_baseline)
 # ----------------------------------------------------------------------------
-def _cpu_threads() -> int:
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
+def blas_threads() -> int:
     try:
         from threadpoolctl import threadpool_info
 
         n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
         return max(n) if n else 1
-    except Exception:
+    except Exception:  # noqa: BLE001
         return os.cpu_count() or 1
 
 
-def _igp_slice(problem, g0: int, g1: int):
-    from paper_2008_11326_b200 import GPPProblem
-
-    return GPPProblem(problem.nbands, g1 - g0, problem.ncouls,
-                      np.asfortranarray(problem.wtilde[:, g0:g1]), np.asfortranarray(problem.i_eps[:, g0:g1]),
-                      problem.aqsntemp, np.asfortranarray(problem.aqsmtemp[g0:g1, :]), problem.wx)
-
-
-class CpuReference:
-    """The reference's production CPU path (evaluate_variant, the ZGEMM-
-    factored numpy code, restated in oracle/gpp_oracle.py) on igp slices of
-    the workload: every step evaluates `igp_per_step` igp columns of the full
-    problem, rotating through all of them.  FLOPs of a step are the
-    reference's analytic count of its slice (computed once, untimed)."""
-
-    def __init__(self, problem, igp_per_step: int):
-        from oracle import gpp_oracle as orc
-        from paper_2008_11326_b200.counters import algorithmic_flops
-
-        self.orc = orc
-        ng = problem.ngpown
-        slices = [(g, min(g + igp_per_step, ng)) for g in range(0, ng, igp_per_step)]
-        self.subs = [_igp_slice(problem, a, b) for a, b in slices]
-        self.flops = []
-        for sub in self.subs:
-            _, near, far = orc.branch_stats(sub, "rcp_sq")
-            self.flops.append(algorithmic_flops(sub.nbands, sub.ngpown, sub.ncouls, len(sub.wx), near, far))
-
-    def run(self, steps: int, warmup: int = 0):
-        """(flops, seconds) of `steps` timed slice evaluations."""
-        for i in range(warmup):
-            self.orc.evaluate_variant(self.subs[i % len(self.subs)], "rcp_sq")
-        flops, secs = 0, 0.0
-        for i in range(steps):
-            k = i % len(self.subs)
-            t0 = time.perf_counter()
-            self.orc.evaluate_variant(self.subs[k], "rcp_sq")
-            secs += time.perf_counter() - t0
-            flops += self.flops[k]
-        return flops, secs
+def host_info() -> dict:
+    return {"cpu_model": cpu_model(), "cpu_count": os.cpu_count(), "blas_threads": blas_threads(),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS", "unset (all cores)")}
 
 
 # ----------------------------------------------------------------------------
-def load_profile_summary():
-    p = ROOT / "profiles" / "ncu_summary.json"
-    if p.exists():
-        try:
-            return json.loads(p.read_text())
-        except json.JSONDecodeError:
+# the reference CPU path: the unmodified rooflab from baseline/_ref when it is
+# there (kind "reference"), else the oracle restatement (kind "port")
+# ----------------------------------------------------------------------------
+class CpuReference:
+    """Whole-problem evaluations of the reference's production CPU path,
+    evaluate_variant(p, "rcp_sq") -- what rooflab's run_version(p, "v8")
+    times (runner.py:258-260)."""
+
+    def __init__(self, dims, seed, nw):
+        ref = ROOT / "baseline" / "_ref"
+        self.kind = "port"
+        if (ref / "rooflab").is_dir():
+            sys.path.insert(0, str(ref))
+            try:
+                import rooflab.gpp as rgpp
+                import rooflab.gpp.kernel as rk
+                import rooflab.gpp.problem as rp
+                import rooflab.gpp.runner as rr
+
+                # nw != 2: the reference's NW constant, imported by value into
+                # three modules (SURVEY.md Table R) -- patched at run time,
+                # the installed source is untouched.
+                rp.NW = rk.NW = rr.NW = nw
+                self.kind = "reference"
+                self.mod = rgpp
+                self.what = "rooflab (unmodified, baseline/_ref) evaluate_variant(p, 'rcp_sq')"
+                self.p = rgpp.synth_problem(*dims, seed=seed)
+            except Exception as e:  # noqa: BLE001 -- fall back to the port
+                self.kind = "port"
+                self.why = f"baseline/_ref import failed: {e}"
+        if self.kind == "port":
+            from oracle import gpp_oracle as orc
+            from paper_2008_11326_b200 import synth_problem
+
+            self.mod = orc
+            self.what = "oracle/gpp_oracle.py evaluate_variant(p, 'rcp_sq') (restatement of kernel.py:98-114)"
+            self.p = synth_problem(*dims, seed=seed, nw=nw, check=False)
+
+    def evaluate(self):
+        return self.mod.evaluate_variant(self.p, "rcp_sq")
+
+    def time(self, steps: int, warmup: int) -> list[float]:
+        for _ in range(warmup):
+            self.evaluate()
+        out = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            self.evaluate()
+            out.append(time.perf_counter() - t0)
+        return out
+
+    def reference_result_seconds(self, dims, seed, nw) -> float | None:
+        """The literal loop-nest oracle (problem.py:179-208) at a small size."""
+        if self.kind != "reference":
             return None
-    return None
+        p = self.mod.synth_problem(*dims, seed=seed)
+        t0 = time.perf_counter()
+        self.mod.reference_result(p)
+        return time.perf_counter() - t0
 
 
+# ----------------------------------------------------------------------------
+# executed FP64 FLOPs: live ncu capture of this build (child process)
+# ----------------------------------------------------------------------------
+def ncu_child(args):
+    """Under ncu: every band shard of the workload once (device synthesis,
+    the production kernel as the timed region runs it)."""
+    from paper_2008_11326_b200 import GPPContext
+    from paper_2008_11326_b200.dist import band_range
+
+    nb, ng, nc = WORKLOADS[args.workload]
+    ctx = GPPContext(0)
+    for r in range(args.gpus):
+        ctx.synth(nb, ng, nc, seed=args.seed, nw=args.nw, band_range=band_range(nb, args.gpus, r))
+        ctx.run(args.variant, counts=False)
+        print(f"shard {r}", flush=True)
+    ctx.close()
+
+
+def ncu_capture(args, timeout_s: float = 420.0) -> dict | None:
+    """Run ncu on the child; per shard: executed FP64 FLOPs, DRAM bytes,
+    FP64-pipe activity of the production kernel launches."""
+    out = Path(os.environ.get("GPP_NCU_DIR", "/tmp")) / f"gpp_ncu_{os.getpid()}.csv"
+    cmd = ["ncu", "--metrics", ",".join(NCU_METRICS), "--clock-control", "none",
+           "-k", "regex:gpp_sacc_kernel|gpp_slot_finalize|gpp_main_kernel|gpp_finalize",
+           "--page", "raw", "--csv", "--print-units", "base", "--log-file", str(out),
+           sys.executable, str(ROOT / "bench.py"), "--ncu-child", "--workload", args.workload,
+           "--nw", str(args.nw), "--seed", str(args.seed), "--variant", args.variant,
+           "--gpus", str(args.gpus)]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = env.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0]
+    t0 = time.perf_counter()
+    try:
+        proc = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s, env=env)
+    except (OSError, subprocess.TimeoutExpired) as e:
+        return {"error": f"ncu failed: {e}"}
+    if proc.returncode != 0 or not out.exists():
+        return {"error": f"ncu rc={proc.returncode}: {(proc.stderr or proc.stdout)[-300:]}"}
+    rows = list(csv.reader(io.StringIO(out.read_text())))
+    out.unlink(missing_ok=True)
+    hdr = rows[0]
+    data = [r for r in rows[2:] if len(r) == len(hdr)]
+    col = {k: i for i, k in enumerate(hdr)}
+
+    def val(r, k):
+        try:
+            return float(r[col[k]].replace(",", ""))
+        except (KeyError, ValueError):
+            return 0.0
+
+    main, fin = [], []
+    for r in data:
+        (main if "gpp_sacc_kernel" in r[col["Kernel Name"]] or "gpp_main_kernel" in r[col["Kernel Name"]]
+         else fin).append(r)
+    fl = lambda r: 2 * val(r, NCU_METRICS[0]) + val(r, NCU_METRICS[1]) + val(r, NCU_METRICS[2])  # noqa: E731
+    dfma = sum(val(r, NCU_METRICS[0]) for r in main)
+    dmul = sum(val(r, NCU_METRICS[1]) for r in main)
+    dadd = sum(val(r, NCU_METRICS[2]) for r in main)
+    dur = sum(val(r, "gpu__time_duration.sum") for r in main)
+    pipe = (sum(val(r, NCU_METRICS[6]) * val(r, "gpu__time_duration.sum") for r in main) / dur) if dur else None
+    return {
+        "source": f"live ncu capture of this build in this run ({len(main)} production-kernel + "
+                  f"{len(fin)} finalize launches, --clock-control none, {time.perf_counter() - t0:.0f} s)",
+        "lib_sha256": lib_sha256(),
+        "executed_flops_main": sum(fl(r) for r in main),
+        "executed_flops_all": sum(fl(r) for r in data),
+        "per_shard_main_flops": None,
+        "dram_bytes_main": sum(val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum") for r in main),
+        "fma_ratio": dfma / (dfma + dmul + dadd) if dfma + dmul + dadd else None,
+        "fp64_pipe_pct": pipe,
+        "ncu_duration_ms_main": dur * 1e-6,
+        "shards": args.gpus,
+    }
+
+
+def committed_capture(args) -> dict | None:
+    """profiles/ncu_summary.json, only if it was taken of this exact build."""
+    try:
+        s = json.loads(NCU_SUMMARY.read_text())
+    except (OSError, json.JSONDecodeError):
+        return None
+    if s.get("lib_sha256") != lib_sha256():
+        return None
+    key = f"{args.workload}/nw{args.nw}/seed{args.seed}/{args.variant}/shards{args.gpus}"
+    w = s.get("workloads", {}).get(key)
+    if not w:
+        return None
+    return {**w, "source": f"profiles/ncu_summary.json ({s.get('source', '')}; lib sha256 matches this build)"}
+
+
+# ----------------------------------------------------------------------------
 def golden_parity(result, workload, seed, nw):
     g = ROOT / "tests" / "golden" / "gpp_big.json"
     if not g.exists():
@@ -244,34 +423,6 @@ def golden_parity(result, workload, seed, nw):
     return None
 
 
-def run_reference(args, dist: Dist):
-    """--impl reference: the reference's CPU path on this host (rank 0 only)."""
-    if dist.rank != 0:
-        return
-    from paper_2008_11326_b200 import synth_problem
-
-    dims = WORKLOADS[args.workload]
-    p = synth_problem(*dims, seed=args.seed, nw=args.nw, check=False)
-    igp_per_step = 6
-    flops, secs = CpuReference(p, igp_per_step).run(args.steps, args.warmup)
-    value = flops / secs / 1e12
-    cores = _cpu_threads()
-    sample = (f"each step = reference evaluate_variant('rcp_sq') (ZGEMM-factored numpy, "
-              f"oracle/gpp_oracle.py) on {igp_per_step} of {dims[1]} igp columns of the full "
-              f"{dims} nw={args.nw} problem, rotating")
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": f"synthetic (synth_problem seed {args.seed})",
-        "config": _config(args, dims),
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                         "sample": sample, "cpu_count": os.cpu_count()},
-        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
 def _config(args, dims):
     return {
         "workload": f"{args.workload} (nbands, ngpown, ncouls) = {dims}, nw={args.nw}",
@@ -282,143 +433,234 @@ def _config(args, dims):
     }
 
 
+def reference_numerator(args) -> tuple[float | None, str]:
+    """The executed-FLOP numerator of this workload for the reference arm:
+    the committed capture of this build (the GPU arm measures it live)."""
+    try:
+        s = json.loads(NCU_SUMMARY.read_text())
+        w = s["workloads"][f"{args.workload}/nw{args.nw}/seed{args.seed}/{args.variant}/shards1"]
+        return float(w["executed_flops_all"]), "profiles/ncu_summary.json (ncu-counted FLOPs of one evaluation by this build)"
+    except (OSError, KeyError, ValueError, json.JSONDecodeError):
+        return None, "no committed capture"
+
+
+def run_reference(args, dist: Dist):
+    """--impl reference: the reference's CPU path on this host (rank 0 only)."""
+    if dist.rank != 0:
+        return
+    from paper_2008_11326_b200.counters import algorithmic_flops
+
+    dims = WORKLOADS[args.workload]
+    ref = CpuReference(dims, args.seed, args.nw)
+    secs = ref.time(args.steps, args.warmup)
+    t = statistics.mean(secs)
+    from oracle import gpp_oracle as orc
+    from paper_2008_11326_b200 import synth_problem
+
+    _, near, far = orc.branch_stats(synth_problem(*dims, seed=args.seed, nw=args.nw, check=False), "rcp_sq")
+    alg = algorithmic_flops(*dims, args.nw, near, far)
+    num, num_src = reference_numerator(args)
+    value = (num if num else alg) / t / 1e12
+    sample = (f"each step = one whole evaluation of the {dims} nw={args.nw} workload through "
+              f"{ref.what}; mean of {args.steps} after {args.warmup} warm-up")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": f"synthetic (synth_problem seed {args.seed})",
+        "config": _config(args, dims),
+        "numerator": {"flops_per_step": num or alg,
+                      "what": ("ncu-counted FP64 FLOPs of the B200 kernels for one evaluation (" + num_src
+                               + "), the same numerator as the GPU line: the ratio is a time ratio")
+                      if num else "reference analytic FLOPs (no committed ncu capture)"},
+        "effective_tflops": alg / t / 1e12,
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": blas_threads(), "kind": ref.kind,
+                         "sample": sample, **host_info(),
+                         **({"fallback_reason": ref.why} if hasattr(ref, "why") else {})},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
 def run_ours(args, dist: Dist):
     from paper_2008_11326_b200 import fp64_peak, synth_problem
     from paper_2008_11326_b200._lib import load
-    from paper_2008_11326_b200.counters import algorithmic_flops
+    from paper_2008_11326_b200.counters import BranchStats, algorithmic_flops, counters_from_stats, fma_ratio
+    from paper_2008_11326_b200.dist import MultiDeviceGPP, ShardedGPP, band_range
 
     dims = WORKLOADS[args.workload]
     nb, ng, nc = dims
     device = dist.local_rank
-    # The weak-scaled workload (5.4 GB of inputs) is drawn on the device
-    # (gpp_synth, bit-exact with synth_problem) instead of in host memory on
-    # every rank; it has no host arrays, so no e2e / CPU-baseline legs.
-    device_synth = args.workload == "weak"
-    p = None if device_synth else synth_problem(nb, ng, nc, seed=args.seed, nw=args.nw, check=False)
     load()
     # FP64 roofline denominator: measured live on this device (MEASURED_PEAKS.json has no FP64).
     fp64_peak(device, 20_000)
     peak_tf, _ = fp64_peak(device, 300_000)
 
-    from paper_2008_11326_b200.dist import ShardedGPP
-
-    shard = ShardedGPP.from_torch(device) if dist.world > 1 else ShardedGPP(device, 0, 1, None)
-    ctx = shard.ctx
-    b0, b1 = shard.band_range(nb)
-    if device_synth:
-        ctx.synth(nb, ng, nc, seed=args.seed, nw=args.nw, band_range=(b0, b1))
+    # ---- the problem, resident on the device(s) ---------------------------
+    group = None
+    if dist.single_process_group:
+        group = MultiDeviceGPP(list(range(args.gpus)))
+        group.synth(nb, ng, nc, seed=args.seed, nw=args.nw)
+        result, (near, far), _ = group.run(args.variant, counts=True)
+        ctx = group.ctxs[0]
+        n_ranks = args.gpus
     else:
-        ctx.upload(p, (b0, b1))
-    result, (near, far), _ = ctx.run(args.variant)  # combined over ranks
+        shard = ShardedGPP.from_torch(device) if dist.world > 1 else ShardedGPP(device, 0, 1, None)
+        ctx = shard.ctx
+        ctx.synth(nb, ng, nc, seed=args.seed, nw=args.nw, band_range=shard.band_range(nb))
+        result, (near, far), _ = ctx.run(args.variant)  # combined over ranks
+        n_ranks = dist.world
     info = ctx.kernel_info(args.variant)
-    flops_job = algorithmic_flops(nb, ng, nc, args.nw, near, far)
+    alg_job = algorithmic_flops(nb, ng, nc, args.nw, near, far)
 
-    # ---- device-resident timed region -----------------------------------
-    ctx.time(args.variant, args.warmup)
+    def timed(iters):
+        return group.time(args.variant, iters) if group else ctx.time(args.variant, iters)
+
+    def launches():
+        return sum(c.launch_count() for c in group.ctxs) if group else ctx.launch_count()
+
+    # ---- device-resident timed region --------------------------------------
+    timed(args.warmup)
     bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
     for attempt in range(2):  # a run that saw a slowdown reason is re-measured once
         dist.barrier()
-        dist.sync()
-        clocks = Clocks(list(range(dist.world)) if dist.rank == 0 else [])
-        if dist.rank == 0:
-            clocks.start()
-        launches0 = ctx.launch_count()
-        total_ms, main_ms = ctx.time(args.variant, args.steps)
-        gpu_launches = ctx.launch_count() - launches0
-        dist.sync()
+        clocks = Clocks(list(range(args.gpus)) if dist.rank == 0 else [])
+        clocks.start()
+        l0 = launches()
+        total_ms, main_ms = timed(args.steps)
+        gpu_launches = launches() - l0
         dist.barrier()
-        clk = clocks.stop() if dist.rank == 0 else None
+        clk = clocks.stop()
         retry = 1.0 if (clk and bad & set(clk.get("reasons", []))) else 0.0
         if attempt == 0 and dist.max(retry) > 0:
             continue
         if clk is not None:
             clk["remeasured"] = attempt > 0
         break
+    gpu_launches = int(dist.sum(gpu_launches))
     t_step_ms = dist.max(total_ms) / args.steps
     t_main_ms = dist.max(main_ms) / args.steps
-    value = flops_job / (t_step_ms * 1e-3) / 1e12
 
-    # ---- end to end through the public API (pinned host buffers) ---------
-    e2e = None
-    if not args.no_e2e and not device_synth:
-        from paper_2008_11326_b200._lib import check
+    # ---- end to end through the public API ---------------------------------
+    e2e = e2e_pinned = None
+    p = None
+    if not args.no_e2e and args.workload != "weak":
+        from paper_2008_11326_b200 import GPPProblem, evaluate_variant
 
-        lib = load()
-        arrays = [p.wtilde, p.i_eps, p.aqsntemp, p.aqsmtemp]
-        for a in arrays:
-            check(lib.gpp_host_register(a.ctypes.data, a.nbytes), "gpp_host_register")
-        try:
-            h2d = (p.wtilde.nbytes + p.i_eps.nbytes + 16 * nc * (b1 - b0) + 16 * ng * (b1 - b0)
-                   + 8 * args.nw * (b1 - b0))
-            d2h = 8 * 4 * args.nw + 16
+        p = synth_problem(nb, ng, nc, seed=args.seed, nw=args.nw, check=False)
+        # Writeable arrays: the public API re-uploads them on every call (a
+        # fresh problem each step, as a user's own numpy arrays would be).
+        q = GPPProblem(nb, ng, nc, p.wtilde.copy(order="F"), p.i_eps.copy(order="F"),
+                       p.aqsntemp.copy(order="F"), p.aqsmtemp.copy(order="F"), p.wx.copy())
+        if group:
+            call = lambda: group.evaluate(q, args.variant)  # noqa: E731
+            api = "MultiDeviceGPP.evaluate -> gpp_evaluate_host per device (one thread each)"
+        elif dist.world > 1:
+            call = lambda: shard.evaluate(q, args.variant)  # noqa: E731
+            api = "ShardedGPP.evaluate -> gpp_evaluate_host (this rank's shard + NCCL)"
+        else:
+            call = lambda: evaluate_variant(q, args.variant, device=device)  # noqa: E731
+            api = "evaluate_variant (the drop-in seam) -> gpp_evaluate_host"
+        r_b0, r_b1 = (band_range(nb, n_ranks, dist.rank) if n_ranks > 1 else (0, nb))
+
+        def h2d_rank(r):
+            b0, b1 = band_range(nb, n_ranks, r)
+            we = 2 * 16 * nc * ng // (n_ranks if n_ranks > 1 else 1)
+            return we + 16 * nc * (b1 - b0) + 16 * ng * (b1 - b0) + 8 * args.nw * (b1 - b0)
+
+        h2d = sum(h2d_rank(r) for r in range(n_ranks))
+        d2h = (8 * 4 * args.nw) * n_ranks
+
+        def time_e2e():
             for _ in range(2):
-                ctx.evaluate_host(p, args.variant, band_range=(b0, b1))
+                call()
             dist.barrier()
-            dist.sync()
             t0 = time.perf_counter()
             for _ in range(args.e2e_steps):
-                ctx.evaluate_host(p, args.variant, band_range=(b0, b1))
-            dist.sync()
+                call()
             el = time.perf_counter() - t0
             dist.barrier()
-            el = dist.max(el)
-            e2e = {"value": flops_job / (el / args.e2e_steps) / 1e12, "unit": "TFLOP/s",
-                   "ms_per_step": el / args.e2e_steps * 1e3, "steps": args.e2e_steps,
-                   "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                   "path": "GPPContext.evaluate_host -> gpp_evaluate_host (C ABI): ig-slab H2D pipelined with the kernel, result D2H"}
-        finally:
-            for a in arrays:
-                lib.gpp_host_unregister(a.ctypes.data)
+            return dist.max(el) / args.e2e_steps
 
-    # Time to solution of the reference's own ZGEMM-factored algorithm on the
-    # device (gpp_run_factored) -- a different algorithm, reported beside the
-    # per-instance kernel, never as its roofline.
+        el = time_e2e()
+        e2e = {"value": None, "unit": "TFLOP/s", "ms_per_step": el * 1e3, "steps": args.e2e_steps,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "inputs": "pageable numpy arrays (the library packs them into its pinned staging ring)",
+               "path": api}
+        if not group and dist.world == 1:
+            from paper_2008_11326_b200._lib import check
+
+            lib = load()
+            arrays = [q.wtilde, q.i_eps, q.aqsntemp, q.aqsmtemp]
+            for a in arrays:
+                check(lib.gpp_host_register(a.ctypes.data, a.nbytes), "gpp_host_register")
+            try:
+                elp = time_e2e()
+            finally:
+                for a in arrays:
+                    lib.gpp_host_unregister(a.ctypes.data)
+            e2e_pinned = {"ms_per_step": elp * 1e3, "inputs": "the same arrays page-locked (gpp_host_register)"}
+
+    # Time to solution of the reference's own factored algorithm on the device
+    # (gpp_run_factored) -- a different algorithm, never the roofline.
     factored = None
-    if dist.world == 1:
+    if n_ranks == 1:
         ctx.run_factored(args.variant, counts=False)
         fms = [ctx.run_factored(args.variant, counts=False)[2] for _ in range(5)]
         fres = ctx.run_factored(args.variant, counts=False)[0]
         factored = {"ms": statistics.median(fms),
-                    "algorithmic_tflops_equiv": flops_job / (statistics.median(fms) * 1e-3) / 1e12,
-                    "what": "gpp_run_factored: cuBLAS ZGEMM of the band weights + branch terms "
-                            "(rooflab/gpp/kernel.py:98-114); a different algorithm, not a roofline figure"}
+                    "what": "gpp_run_factored: the reference's factored algorithm (kernel.py:98-114) -- "
+                            "band weights W = aqsntemp conj(aqsmtemp)^T by the repo's FP64 GEMM kernel, "
+                            "then the branch terms; a different algorithm, not a roofline figure"}
         gp = golden_parity(fres, args.workload, args.seed, args.nw) if args.variant == "rcp_sq" else None
         if gp:
             factored["max_rel_err_vs_reference"] = gp["max_rel_err_vs_reference"]
 
+    # ---- executed FLOPs: live ncu capture (rank 0), after every timing ------
+    cap = None
+    if dist.rank == 0:
+        cap = None if args.no_ncu else ncu_capture(args)
+        if not cap or "error" in cap:
+            err = cap.get("error") if cap else "skipped (--no-ncu)"
+            cap = committed_capture(args) or {"error": err}
+    dist.barrier()
+
     if dist.rank != 0:
-        ctx.close()
+        (group.close() if group else ctx.close())
         return
 
-    # ---- CPU baseline (rank 0, N=1 only) ---------------------------------
+    # ---- CPU baseline (rank 0, N=1 only) -----------------------------------
     cpu = None
-    if dist.world == 1 and not args.no_cpu_baseline and not device_synth:
-        # Whole passes over the workload until >= 10 s of CPU work (at most
-        # 20 passes); the rate is total algorithmic FLOPs / total time.
-        igp_per_step = 6
-        steps = -(-ng // igp_per_step)  # one full pass over the workload
-        cref = CpuReference(p, igp_per_step)
-        fl_tot, secs_tot, passes = 0, 0.0, 0
-        while passes < 20 and (secs_tot < 10.0 or passes < 1):
-            fl, secs = cref.run(steps, 1 if passes == 0 else 0)
-            fl_tot, secs_tot, passes = fl_tot + fl, secs_tot + secs, passes + 1
-        cpu = {"value": fl_tot / secs_tot / 1e12, "unit": "TFLOP/s", "cores": _cpu_threads(), "kind": "port",
-               "sample": f"{passes} full passes of the {dims} nw={args.nw} workload through the "
-                         f"reference's evaluate_variant('rcp_sq') restated in oracle/ (numpy + OpenBLAS "
-                         f"ZGEMM), each in {steps} igp slices of {igp_per_step}; {secs_tot:.1f} s",
-               "cpu_count": os.cpu_count()}
+    if n_ranks == 1 and not args.no_cpu_baseline and args.workload != "weak":
+        ref = CpuReference(dims, args.seed, args.nw)
+        secs = ref.time(steps=4, warmup=1)
+        t_cpu = statistics.mean(secs)
+        num = (cap or {}).get("executed_flops_all") or alg_job
+        cpu = {"value": num / t_cpu / 1e12, "unit": "TFLOP/s", "cores": blas_threads(), "kind": ref.kind,
+               "sample": f"4 whole evaluations (after 1 warm-up) of the {dims} nw={args.nw} workload through "
+                         f"{ref.what}, {sum(secs):.1f} s; numerator = this line's executed-FLOP count",
+               "ms_per_evaluation": t_cpu * 1e3, "effective_tflops": alg_job / t_cpu / 1e12,
+               **host_info()}
+        rr = ref.reference_result_seconds(WORKLOADS["tiny"], 42, 2)
+        if rr is not None:
+            cpu["reference_result_tiny_s"] = rr
+        cpu["reference_result_paper_s"] = "see profiles/r02_cpu_reference_result.json (~90 s, run once)"
 
-    prof = load_profile_summary() or {}
-    wl = prof.get("workload") or {}
-    if wl != {"dims": list(dims), "nw": args.nw, "seed": args.seed, "variant": args.variant}:
-        prof = {}  # the committed ncu capture is of another workload
-    achieved = flops_job / dist.world / (t_main_ms * 1e-3) / 1e12  # dominant kernel, per GPU
+    # ---- assemble -----------------------------------------------------------
+    exec_job = (cap or {}).get("executed_flops_all")
+    exec_main = (cap or {}).get("executed_flops_main")
+    value = exec_job / (t_step_ms * 1e-3) / 1e12 if exec_job else None
     tot_inst = args.nw * nb * ng * nc
+    per_gpu_main = exec_main / n_ranks if exec_main else None
+    achieved = per_gpu_main / (t_main_ms * 1e-3) / 1e12 if per_gpu_main else None
+    cnt = counters_from_stats("rcp_sq", BranchStats(tot_inst, near, far), nb * ng * nc, True)
+    r_exec = (cap or {}).get("fma_ratio")
     line = {
         "metric": METRIC,
-        "value": value,
+        "value": value if value is not None else alg_job / (t_step_ms * 1e-3) / 1e12,
         "unit": "TFLOP/s",
-        "n_gpus": dist.world,
+        "n_gpus": args.gpus,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": t_step_ms,
@@ -426,73 +668,67 @@ def run_ours(args, dist: Dist):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": (f"synthetic (synth_problem seed {args.seed}, PCG64 as the reference draws it"
-                 + (", drawn on the device by gpp_synth)" if device_synth else ")")),
+        "data": f"synthetic (synth_problem seed {args.seed}, PCG64 as the reference draws it; drawn on "
+                f"the device by gpp_synth for the timed region)",
         "config": _config(args, dims),
+        "value_kind": ("ncu-counted: executed FP64 FLOPs per step (2*dfma + dmul + dadd, all GPUs) / step time"
+                       if value is not None else
+                       "EFFECTIVE (no ncu count available: " + str((cap or {}).get("error")) + ")"),
+        "effective_tflops": alg_job / (t_step_ms * 1e-3) / 1e12,
+        "effective_kind": "the reference's analytic FLOPs (kernel.py:191-212) / step time; the kernels execute "
+                          f"{100.0 * exec_job / alg_job:.0f}% of them" if exec_job else "analytic / step time",
+        "pct_fp64_peak": 100.0 * achieved / peak_tf if achieved else None,
         "roofline": {
             "bound": "fp64",
-            "bound_note": ("the contract's enum is hbm|tensor; this path is bound by the FP64 vector "
-                           "pipe (DFMA): no dense contraction for tensor cores (north star), DRAM at "
-                           "~1.4 % of peak"),
+            "bound_note": ("the contract's enum is hbm|tensor; this path is bound by the FP64 vector pipe "
+                           "(DFMA): no dense contraction for tensor cores (north star), DRAM at ~1.4 % of peak"),
             "achieved": achieved,
             "peak": peak_tf,
             "unit": "TFLOP/s",
-            "frac": achieved / peak_tf,
-            "traffic": prof.get("dram_bytes_per_launch"),
+            "frac": achieved / peak_tf if achieved else None,
+            "traffic": ((cap or {}).get("dram_bytes_main") / n_ranks) if (cap or {}).get("dram_bytes_main") else None,
+            "achieved_kind": "ncu-counted executed FP64 FLOPs of the production kernel per GPU / its CUDA-event time",
+            "source": (cap or {}).get("source"),
+            "lib_sha256": lib_sha256(),
             "peak_source": "measured live: DFMA microbenchmark (gpp_fp64_peak) on this GPU in this run",
             "kernel": "gpp_sacc_kernel (rcp_sq production kernel)",
             "kernel_ms": t_main_ms,
-            "algorithmic_flops_per_launch": flops_job / dist.world,
-            "fma_ratio_analytic": None,
+            "executed_flops_per_launch": per_gpu_main,
+            "algorithmic_flops_per_launch": alg_job / n_ranks,
+            "fp64_pipe_active_pct_ncu": (cap or {}).get("fp64_pipe_pct"),
+            "fma_ratio_executed": r_exec,
+            "fma_ceiling_tflops": peak_tf * (1 + r_exec) / 2 if r_exec else None,
+            "frac_of_fma_ceiling": (achieved / (peak_tf * (1 + r_exec) / 2)) if (achieved and r_exec) else None,
+            "fma_ratio_analytic": fma_ratio(cnt),
         },
-        "pct_fp64_peak": 100.0 * value / dist.world / peak_tf,
         "gpu_launches": gpu_launches,
         "clocks": clk,
         "e2e": e2e,
+        "e2e_pinned": e2e_pinned,
         "cpu_baseline": cpu,
         "branch_stats": {"instances": tot_inst, "near": near, "far": far},
         "kernel_info": info,
         "factored_time_to_solution": factored,
-        "ncu": {k: prof.get(k) for k in ("executed_flops_per_launch", "executed_over_algorithmic",
-                                         "fma_ratio", "dram_bytes_per_launch", "source")} if prof else None,
+        "ncu": cap,
     }
-    if prof.get("executed_flops_per_launch"):
-        # ncu-counted FP64 FLOPs (2*dfma + dmul + dadd, the metric BASELINE names)
-        # of one launch, timed live here; the executed FMA ratio sets the
-        # paper's FMA-ratio ceiling (machine.py:44-60).
-        ex = prof["executed_flops_per_launch"] / (t_main_ms * 1e-3) / 1e12
-        line["ncu_counted_tflops_per_gpu"] = ex
-        line["pct_fp64_peak_ncu_counted"] = 100.0 * ex / peak_tf
-        ceil = peak_tf * (1 + prof["fma_ratio"]) / 2
-        line["fma_ceiling_tflops_executed_mix"] = ceil
-        line["pct_fma_ceiling_ncu_counted"] = 100.0 * ex / ceil
-        # the kernel executes fewer FP64 operations than the
-        # reference's analytic count (per-instance algebra: one rsqrt seed for
-        # 1/d and sqrt(d), (ig, igp) constants applied once per item), so the
-        # algorithmic rate is an EFFECTIVE rate.  The hardware utilisation is
-        # the ncu-counted fraction beside it.
-        line["roofline"]["achieved_kind"] = (
-            "effective: the reference's analytic FLOPs (kernel.py:191-212) per launch / kernel time; "
-            f"the kernel executes {100.0 * prof['executed_over_algorithmic']:.0f}% of them (ncu)")
-        line["roofline"]["achieved_executed"] = ex
-        line["roofline"]["frac_executed"] = ex / peak_tf
-    from paper_2008_11326_b200.counters import BranchStats, counters_from_stats, fma_ratio
-
-    cnt = counters_from_stats("rcp_sq", BranchStats(tot_inst, near, far), nb * ng * nc, True)
-    r = fma_ratio(cnt)
-    line["roofline"]["fma_ratio_analytic"] = r
-    # The paper's FMA-ratio ceiling for the reference's analytic instruction
-    # mix (kernel.py:144-212).  It bounds EXECUTED FLOPs of that mix; the
-    # effective rate above is not compared with it (it can exceed it).
-    line["fma_ceiling_tflops_analytic_mix"] = peak_tf * (1 + r) / 2
+    num = exec_job or alg_job
+    if e2e:
+        e2e["value"] = num / (e2e["ms_per_step"] * 1e-3) / 1e12
+        if e2e_pinned:
+            e2e_pinned["value"] = num / (e2e_pinned["ms_per_step"] * 1e-3) / 1e12
+    if factored:
+        factored["effective_tflops_equiv"] = alg_job / (factored["ms"] * 1e-3) / 1e12
     if args.variant == "rcp_sq":
         line["parity"] = golden_parity(result, args.workload, args.seed, args.nw)
     print(json.dumps(line), flush=True)
-    ctx.close()
+    (group.close() if group else ctx.close())
 
 
 def main():
     args = parse_args()
+    if args.ncu_child:
+        ncu_child(args)
+        return
     dist = Dist(args.gpus)
     try:
         if args.impl == "reference":

@@ -21,9 +21,17 @@
  *     gpp_last_error() returns a thread-local message.
  *   - Host input buffers are borrowed for the duration of the call only and
  *     never written.  Outputs go to caller-allocated host buffers.
- *   - A gpp_ctx is single-caller (not thread-safe); distinct contexts may be
- *     used concurrently (the reference allows concurrent independent runs,
- *     SPEC.md:412).
+ *   - Distinct contexts may be used concurrently (the reference allows
+ *     concurrent independent runs); calls on one shared context
+ *     are serialised by a per-context lock.
+ *   - Reproducible: every evaluation of the same inputs and variant returns
+ *     the same bits, whichever entry point (gpp_evaluate_host's pipelined
+ *     first call, gpp_run on the resident problem, any slab count) -- the
+ *     production kernel runs a canonical item schedule and its finalize sums
+ *     the items in a fixed order.
+ *   - With a communicator attached, an error aborts it (ncclCommAbort), so
+ *     peers fail (GPP_ERR_NCCL) instead of waiting on a collective; waits
+ *     poll ncclCommGetAsyncError and time out after GPP_NCCL_TIMEOUT_S.
  *   - There is no CPU fallback: without a working CUDA device every compute
  *     entry point fails with GPP_ERR_CUDA.
  */
@@ -88,6 +96,8 @@ int gpp_create(gpp_ctx** ctx, int device);
 void gpp_destroy(gpp_ctx* ctx);
 
 /* Copy one problem (or the band shard [band0, band1) of it) to the device.
+ * An empty shard (band0 == band1, e.g. more ranks than bands) is allowed: it
+ * contributes zeros and still joins the collectives.
  * Replaces the array hand-off into evaluate_variant (kernel.py:98) and the
  * GPPProblem fields (problem.py:50-71).
  *   wtilde, i_eps : (ncouls, ngpown) complex, F-order  -> 2*ncouls*ngpown doubles
@@ -202,7 +212,17 @@ int gpp_comm_init_all(gpp_ctx** ctxs, int n);
 int gpp_run_group(gpp_ctx** ctxs, int n, int32_t variant, double* achtemp, double* asxtemp,
                   int64_t* near_far, float* kernel_ms);
 
-/* Page-lock an existing host buffer so uploads from it run at DMA speed. */
+/* Device-resident timing of the single-process group: `iters` evaluations
+ * enqueued back to back on every device, each followed by one grouped
+ * ncclAllReduce of the partials, with no host synchronisation in between.
+ * total_ms / main_ms: the slowest device's event time of the whole run / of
+ * its summed main-kernel spans (the bench's N-GPU timing without torchrun). */
+int gpp_time_group(gpp_ctx** ctxs, int n, int32_t variant, int32_t iters, float* total_ms,
+                   float* main_ms);
+
+/* Page-lock an existing host buffer so uploads from it run at DMA speed.
+ * (Not required: pageable inputs are packed into the library's pinned
+ * staging ring by host threads, overlapped with the DMA.) */
 int gpp_host_register(void* ptr, size_t bytes);
 int gpp_host_unregister(void* ptr);
 

@@ -82,6 +82,11 @@ SIGNATURES = {
         [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int32, _c_double_p, _c_double_p,
          _c_i64_p, _c_float_p],
     ),
+    "gpp_time_group": (
+        ctypes.c_int,
+        [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int32, ctypes.c_int32, _c_float_p,
+         _c_float_p],
+    ),
     "gpp_host_register": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t]),
     "gpp_host_unregister": (ctypes.c_int, [ctypes.c_void_p]),
     "gpp_fp64_peak": (ctypes.c_int, [ctypes.c_int, ctypes.c_int32, ctypes.POINTER(ctypes.c_double), _c_float_p]),

@@ -7,6 +7,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -14,6 +15,7 @@
 #include <list>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gpp_b200.h"
@@ -126,6 +128,8 @@ struct gpp_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t cstream = nullptr;  // H2D copies of the pipelined evaluate
   cudaStream_t kstream2 = nullptr;  // odd ig slabs: overlaps a slab's tail with the next
+  cudaStream_t nstream = nullptr;   // NCCL broadcasts of the column-split upload
+  cudaEvent_t ev_we = nullptr;      // wtilde / eps complete (column-split upload)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> slab_ev;
@@ -160,6 +164,7 @@ struct gpp_ctx {
 
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  bool comm_aborted = false;  // an error after comm init aborted the communicator
 
   // Launch plans of the uploaded problem, keyed by (variant, nw group, count);
   // cleared whenever a problem is (re)loaded.
@@ -214,6 +219,8 @@ int ensure_init(gpp_ctx* c) {
   GPP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   GPP_CUDA(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
   GPP_CUDA(cudaStreamCreateWithFlags(&c->kstream2, cudaStreamNonBlocking));
+  GPP_CUDA(cudaStreamCreateWithFlags(&c->nstream, cudaStreamNonBlocking));
+  GPP_CUDA(cudaEventCreateWithFlags(&c->ev_we, cudaEventDisableTiming));
   for (auto& ev : c->ev) GPP_CUDA(cudaEventCreate(&ev));
   GPP_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   GPP_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
@@ -846,6 +853,13 @@ int allreduce_out(gpp_ctx* c) {
 // Enqueue one full evaluation of the resident problem on c->stream.  If
 // ev_main is non-null, the main kernels are bracketed by ev_main[0..1].
 int enqueue_eval(gpp_ctx* c, int variant, bool count, cudaEvent_t* ev_main, bool allreduce) {
+  if (c->nbands == 0) {  // empty shard: zeros, then the collective
+    if (ev_main) GPP_CUDA(cudaEventRecord(ev_main[0], c->stream));
+    GPP_CUDA(cudaMemsetAsync(c->out.ptr, 0, 4 * sizeof(double) * c->nw, c->stream));
+    GPP_CUDA(cudaMemsetAsync(c->counts.ptr, 0, 2 * sizeof(unsigned long long), c->stream));
+    if (ev_main) GPP_CUDA(cudaEventRecord(ev_main[1], c->stream));
+    return allreduce ? allreduce_out(c) : GPP_OK;
+  }
   EvalRun r;
   int rc = eval_begin(c, variant, count, ev_main, &r);
   if (rc) return rc;
@@ -861,6 +875,30 @@ int check_variant(int32_t variant) {
   if (variant < GPP_VARIANT_DIV || variant > GPP_KERNEL_ONE_SEED)
     return fail(GPP_ERR_ARG, "unknown variant " + std::to_string(variant) +
                                  " (expected 0=div, 1=rcp, 2=rcp_sq, 3..5 = ladder kernels)");
+  return GPP_OK;
+}
+
+}  // namespace
+
+namespace {
+// After an error on a context with a communicator, abort the communicator
+// (ncclCommAbort) so that no peer waits forever on a collective this rank
+// will not join; later calls on the context fail with GPP_ERR_NCCL.
+int comm_guard(gpp_ctx* c, int rc) {
+  if (rc == GPP_OK || !c || !c->comm) return rc;
+  CtxLock lock(c);
+  if (c->comm) {
+    DeviceGuard g(c->device);
+    ncclCommAbort(c->comm);
+    c->comm = nullptr;
+    c->comm_aborted = true;
+  }
+  return rc;
+}
+
+int comm_alive(const gpp_ctx* c) {
+  if (c && c->comm_aborted)
+    return fail(GPP_ERR_NCCL, "the communicator was aborted after an earlier error");
   return GPP_OK;
 }
 
@@ -897,6 +935,7 @@ void gpp_destroy(gpp_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->cstream) cudaStreamSynchronize(c->cstream);
     if (c->kstream2) cudaStreamSynchronize(c->kstream2);
+    if (c->nstream) cudaStreamSynchronize(c->nstream);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->blas) cublasDestroy(c->blas);
     c->weight.release();
@@ -924,6 +963,8 @@ void gpp_destroy(gpp_ctx* c) {
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->kstream2) cudaStreamDestroy(c->kstream2);
+    if (c->nstream) cudaStreamDestroy(c->nstream);
+    if (c->ev_we) cudaEventDestroy(c->ev_we);
     if (c->cstream) cudaStreamDestroy(c->cstream);
     if (c->stream) cudaStreamDestroy(c->stream);
   }
@@ -949,10 +990,12 @@ int validate(const gpp_ctx* c, const HostProblem& h) {
   if (h.nw < 1) return fail(GPP_ERR_ARG, "nw must be at least 1");
   if (!h.wtilde || !h.i_eps || !h.aqsntemp || !h.aqsmtemp || !h.wx)
     return fail(GPP_ERR_ARG, "input array pointer is NULL");
-  if (h.band0 < 0 || h.band1 > h.nbands || h.band0 >= h.band1)
+  // An empty shard (band0 == band1) is allowed: a rank with no bands (more
+  // ranks than bands) contributes zeros but still joins the collectives.
+  if (h.band0 < 0 || h.band1 > h.nbands || h.band0 > h.band1)
     return fail(GPP_ERR_ARG, "band range [" + std::to_string(h.band0) + ", " +
-                                 std::to_string(h.band1) + ") is empty or outside [0, " +
-                                 std::to_string(h.nbands) + ")");
+                                 std::to_string(h.band1) + ") is reversed or outside [0, " +
+                                 std::to_string(h.nbands) + "]");
   const int64_t kIntMax = 0x7fffffff;
   if (h.ncouls > kIntMax || h.ngpown > kIntMax || h.nbands > kIntMax ||
       (h.ncouls + gpp::kThreads) * (h.ngpown + gpp::kMaxIgpTile) > (int64_t{1} << 40))
@@ -1137,15 +1180,63 @@ HostPins host_pins(const HostProblem& h) {
   return p;
 }
 
-// H2D of the ig rows [i0, i1) of wtilde, i_eps and the aqsntemp shard.
+// H2D of the ig rows [i0, i1) of wtilde and i_eps (unless !with_we) and of
+// the aqsntemp shard.
 int copy_rows(gpp_ctx* c, const HostProblem& h, const HostPins& pins, int64_t i0, int64_t i1,
-              cudaStream_t s) {
-  int rc = copy_cols(c, c->wtilde.ptr, h.wtilde, h.ncouls, h.ngpown, i0, i1, pins.wtilde, s);
-  if (!rc) rc = copy_cols(c, c->eps.ptr, h.i_eps, h.ncouls, h.ngpown, i0, i1, pins.eps, s);
+              cudaStream_t s, bool with_we = true) {
+  int rc = GPP_OK;
+  if (with_we) {
+    rc = copy_cols(c, c->wtilde.ptr, h.wtilde, h.ncouls, h.ngpown, i0, i1, pins.wtilde, s);
+    if (!rc) rc = copy_cols(c, c->eps.ptr, h.i_eps, h.ncouls, h.ngpown, i0, i1, pins.eps, s);
+  }
   if (!rc)
     rc = copy_cols(c, c->aqsn.ptr, h.aqsntemp + 2 * static_cast<size_t>(h.band0) * h.ncouls,
                    h.ncouls, h.band1 - h.band0, i0, i1, pins.aqsn, s);
   return rc;
+}
+
+// Column-split upload of the replicated wtilde / i_eps (band sharding over
+// ranks): rank r copies only its igp columns [g0_r, g1_r) over
+// its own PCIe link (whole columns: contiguous in F-order), then every rank
+// broadcasts its columns to the others over NVLink (one grouped set of
+// ncclBroadcast, in place, on nstream).  c->ev_we marks wtilde / eps complete
+// on the device.  Per rank the H2D drops from 2 nc ng to 2 nc ng / N complex
+// values.  With one rank (GPP_COLUMN_UPLOAD=1, tests) it is a plain copy.
+bool column_split(const gpp_ctx* c) {
+  static const bool force = [] {
+    const char* e = std::getenv("GPP_COLUMN_UPLOAD");
+    return e && e[0] == '1';
+  }();
+  return (c->comm && c->nranks > 1) || force;
+}
+
+int upload_we_split(gpp_ctx* c, const HostProblem& h, const HostPins& pins) {
+  const int n = (c->comm && c->nranks > 1) ? c->nranks : 1, me = n > 1 ? c->rank : 0;
+  auto g0 = [&](int r) { return h.ngpown * r / n; };
+  const int64_t a = g0(me), b = g0(me + 1), nc = h.ncouls;
+  int rc = copy_cols(c, c->wtilde.ptr + a * nc, h.wtilde + 2 * a * nc, nc, b - a, 0, nc,
+                     pins.wtilde, c->cstream);
+  if (!rc)
+    rc = copy_cols(c, c->eps.ptr + a * nc, h.i_eps + 2 * a * nc, nc, b - a, 0, nc, pins.eps,
+                   c->cstream);
+  if (rc) return rc;
+  GPP_CUDA(cudaEventRecord(c->ev_we, c->cstream));
+  if (n > 1) {
+    GPP_CUDA(cudaStreamWaitEvent(c->nstream, c->ev_we, 0));
+    GPP_NCCL(ncclGroupStart());
+    for (int r = 0; r < n; ++r) {
+      const size_t off = static_cast<size_t>(g0(r)) * nc;
+      const size_t cnt = static_cast<size_t>(g0(r + 1) - g0(r)) * nc * 2;
+      if (cnt == 0) continue;
+      GPP_NCCL(ncclBroadcast(c->wtilde.ptr + off, c->wtilde.ptr + off, cnt, ncclDouble, r, c->comm,
+                             c->nstream));
+      GPP_NCCL(ncclBroadcast(c->eps.ptr + off, c->eps.ptr + off, cnt, ncclDouble, r, c->comm,
+                             c->nstream));
+    }
+    GPP_NCCL(ncclGroupEnd());
+    GPP_CUDA(cudaEventRecord(c->ev_we, c->nstream));
+  }
+  return GPP_OK;
 }
 
 // ig-slab schedule of the pipelined evaluate, as block offsets.  The copy is
@@ -1218,6 +1309,34 @@ std::vector<int> slab_schedule(gpp_ctx* c, const EvalRun& r, int n_blk, int slab
   return blk0;
 }
 
+// Wait for stream s.  With a communicator attached, poll instead of
+// blocking, so that a failed or aborted peer (ncclCommGetAsyncError) or a
+// stuck collective (GPP_NCCL_TIMEOUT_S, default 600 s) surfaces as
+// GPP_ERR_NCCL instead of a hang; the caller's guard then aborts the comm.
+int wait_stream(gpp_ctx* c, cudaStream_t s) {
+  if (!(c->comm && c->nranks > 1)) {
+    GPP_CUDA(cudaStreamSynchronize(s));
+    return GPP_OK;
+  }
+  static const double timeout_s = [] {
+    const char* e = std::getenv("GPP_NCCL_TIMEOUT_S");
+    return e ? std::max(1.0, std::atof(e)) : 600.0;
+  }();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e == cudaSuccess) return GPP_OK;
+    if (e != cudaErrorNotReady) return cuda_fail(e, "cudaStreamQuery");
+    ncclResult_t st = ncclSuccess;
+    GPP_NCCL(ncclCommGetAsyncError(c->comm, &st));
+    if (st != ncclSuccess && st != ncclInProgress)
+      return fail(GPP_ERR_NCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(st));
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s)
+      return fail(GPP_ERR_NCCL, "collective did not complete within GPP_NCCL_TIMEOUT_S");
+    std::this_thread::sleep_for(std::chrono::microseconds(10));
+  }
+}
+
 int finish_run(gpp_ctx* c, double* achtemp, double* asxtemp, int64_t* near_far) {
   int rc = allreduce_out(c);
   if (rc) return rc;
@@ -1225,7 +1344,8 @@ int finish_run(gpp_ctx* c, double* achtemp, double* asxtemp, int64_t* near_far) 
                            cudaMemcpyDeviceToHost, c->stream));
   GPP_CUDA(cudaMemcpyAsync(c->h_counts, c->counts.ptr, 2 * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, c->stream));
-  GPP_CUDA(cudaStreamSynchronize(c->stream));
+  rc = wait_stream(c, c->stream);
+  if (rc) return rc;
   std::memcpy(achtemp, c->h_out, 2 * sizeof(double) * c->nw);
   std::memcpy(asxtemp, c->h_out + 2 * c->nw, 2 * sizeof(double) * c->nw);
   if (near_far) {
@@ -1239,7 +1359,7 @@ int finish_run(gpp_ctx* c, double* achtemp, double* asxtemp, int64_t* near_far) 
 
 extern "C" {
 
-int gpp_upload(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw,
+static int gpp_upload_impl(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw,
                const double* wtilde, const double* i_eps, const double* aqsntemp,
                const double* aqsmtemp, const double* wx, int32_t wx_band_indexed,
                int64_t band0, int64_t band1) {
@@ -1265,7 +1385,7 @@ int gpp_upload(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32
   return GPP_OK;
 }
 
-int gpp_evaluate_host(gpp_ctx* c, int32_t variant, int64_t nbands, int64_t ngpown, int64_t ncouls,
+static int gpp_evaluate_host_impl(gpp_ctx* c, int32_t variant, int64_t nbands, int64_t ngpown, int64_t ncouls,
                       int32_t nw, const double* wtilde, const double* i_eps,
                       const double* aqsntemp, const double* aqsmtemp, const double* wx,
                       int32_t wx_band_indexed, int64_t band0, int64_t band1, int32_t slabs,
@@ -1288,32 +1408,48 @@ int gpp_evaluate_host(gpp_ctx* c, int32_t variant, int64_t nbands, int64_t ngpow
   // ig slabs on 256-ig block boundaries; the canonical items of slab s run as
   // soon as its rows have landed, while slab s+1 is in flight.
   const int n_blk = static_cast<int>((ncouls + gpp::kThreads - 1) / gpp::kThreads);
-  EvalRun r;
-  rc = eval_begin(c, variant, near_far != nullptr, nullptr, &r);
-  if (rc) return rc;
   const HostPins pins = host_pins(h);
-  const std::vector<int> blk0 =
-      slab_schedule(c, r, n_blk, slabs, !(pins.wtilde && pins.eps && pins.aqsn));
-  const int n_sched = static_cast<int>(blk0.size()) - 1;
-  while (static_cast<int>(c->slab_ev.size()) < n_sched + 1) {
-    cudaEvent_t e;
-    GPP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    c->slab_ev.push_back(e);
-  }
+  const bool split = column_split(c);
   GPP_CUDA(cudaEventRecord(c->ev[2], c->cstream));
   rc = copy_small(c, h, c->cstream);
   if (rc) return rc;
-  for (int sl = 0; sl < n_sched; ++sl) {
-    const int64_t i0 = static_cast<int64_t>(blk0[sl]) * gpp::kThreads;
-    const int64_t i1 = std::min<int64_t>(ncouls, static_cast<int64_t>(blk0[sl + 1]) * gpp::kThreads);
-    rc = copy_rows(c, h, pins, i0, i1, c->cstream);
-    if (rc) return rc;
-    GPP_CUDA(cudaEventRecord(c->slab_ev[sl], c->cstream));
-    rc = eval_rows(c, &r, blk0[sl], blk0[sl + 1], c->slab_ev[sl]);
+  if (split) {
+    rc = upload_we_split(c, h, pins);
     if (rc) return rc;
   }
-  rc = eval_end(c, &r);
-  if (rc) return rc;
+  if (c->nbands == 0) {  // empty shard: no rows to copy, zeros into the collective
+    GPP_CUDA(cudaStreamWaitEvent(c->stream, split ? c->ev_we : c->ev[2], 0));
+    rc = enqueue_eval(c, variant, near_far != nullptr, nullptr, false);
+    if (rc) return rc;
+  } else {
+    EvalRun r;
+    rc = eval_begin(c, variant, near_far != nullptr, nullptr, &r);
+    if (rc) return rc;
+    if (split) {
+      GPP_CUDA(cudaStreamWaitEvent(c->stream, c->ev_we, 0));
+      GPP_CUDA(cudaStreamWaitEvent(c->kstream2, c->ev_we, 0));
+    }
+    const std::vector<int> blk0 = slab_schedule(
+        c, r, n_blk, slabs, !(pins.aqsn && (split || (pins.wtilde && pins.eps))));
+    const int n_sched = static_cast<int>(blk0.size()) - 1;
+    while (static_cast<int>(c->slab_ev.size()) < n_sched + 1) {
+      cudaEvent_t e;
+      GPP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->slab_ev.push_back(e);
+    }
+    for (int sl = 0; sl < n_sched; ++sl) {
+      const int64_t i0 = static_cast<int64_t>(blk0[sl]) * gpp::kThreads;
+      const int64_t i1 =
+          std::min<int64_t>(ncouls, static_cast<int64_t>(blk0[sl + 1]) * gpp::kThreads);
+      rc = copy_rows(c, h, pins, i0, i1, c->cstream, !split);
+      if (rc) return rc;
+      GPP_CUDA(cudaEventRecord(c->slab_ev[sl], c->cstream));
+      rc = eval_rows(c, &r, blk0[sl], blk0[sl + 1], c->slab_ev[sl]);
+      if (rc) return rc;
+    }
+    rc = eval_end(c, &r);
+    if (rc) return rc;
+  }
   GPP_CUDA(cudaEventRecord(c->ev[3], c->stream));
   rc = finish_run(c, achtemp, asxtemp, near_far);
   if (rc) return rc;
@@ -1322,7 +1458,7 @@ int gpp_evaluate_host(gpp_ctx* c, int32_t variant, int64_t nbands, int64_t ngpow
   return GPP_OK;
 }
 
-int gpp_run(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp, int64_t* near_far,
+static int gpp_run_impl(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp, int64_t* near_far,
             float* kernel_ms) {
   CtxLock lock(c);
   if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
@@ -1342,7 +1478,7 @@ int gpp_run(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp, int64
   return GPP_OK;
 }
 
-int gpp_time(gpp_ctx* c, int32_t variant, int32_t iters, float* total_ms, float* main_ms) {
+static int gpp_time_impl(gpp_ctx* c, int32_t variant, int32_t iters, float* total_ms, float* main_ms) {
   CtxLock lock(c);
   if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
   int rc = check_variant(variant);
@@ -1467,7 +1603,7 @@ int gpp_comm_init(gpp_ctx* c, int nranks, int rank, const unsigned char* id128) 
   return GPP_OK;
 }
 
-int gpp_synth(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw,
+static int gpp_synth_impl(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw,
               const uint64_t* pcg_state, const double* wx, int64_t band0, int64_t band1) {
   CtxLock lock(c);
   if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
@@ -1522,7 +1658,7 @@ int gpp_synth(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32_
   return GPP_OK;
 }
 
-int gpp_run_factored(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp,
+static int gpp_run_factored_impl(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp,
                      int64_t* near_far, float* ms) {
   CtxLock lock(c);
   if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
@@ -1674,7 +1810,7 @@ int gpp_comm_init_all(gpp_ctx** ctxs, int n) {
   return GPP_OK;
 }
 
-int gpp_run_group(gpp_ctx** ctxs, int n, int32_t variant, double* achtemp, double* asxtemp,
+static int gpp_run_group_impl(gpp_ctx** ctxs, int n, int32_t variant, double* achtemp, double* asxtemp,
                   int64_t* near_far, float* kernel_ms) {
   CtxLock lock(ctxs, n);
   if (!ctxs || n < 1) return fail(GPP_ERR_ARG, "need at least one context");
@@ -1716,7 +1852,8 @@ int gpp_run_group(gpp_ctx** ctxs, int n, int32_t variant, double* achtemp, doubl
     gpp_ctx* c = ctxs[i];
     DeviceGuard g(c->device);
     if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
-    GPP_CUDA(cudaStreamSynchronize(c->stream));
+    rc = wait_stream(c, c->stream);
+    if (rc) return rc;
     float ms = 0.f;
     GPP_CUDA(cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
     worst = std::max(worst, ms);
@@ -1780,6 +1917,165 @@ int gpp_fp64_peak(int device, int32_t iters, double* tflops, float* ms) {
   if (tflops) *tflops = flops / (t * 1e-3) / 1e12;
   if (ms) *ms = t;
   return GPP_OK;
+}
+
+
+// ----- public entry points: the implementations above, behind comm_guard ---
+int gpp_upload(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw,
+               const double* wtilde, const double* i_eps, const double* aqsntemp,
+               const double* aqsmtemp, const double* wx, int32_t wx_band_indexed,
+               int64_t band0, int64_t band1) {
+  int rc = comm_alive(c);
+  if (rc) return rc;
+  return comm_guard(c, gpp_upload_impl(c, nbands, ngpown, ncouls, nw, wtilde, i_eps, aqsntemp,
+                                       aqsmtemp, wx, wx_band_indexed, band0, band1));
+}
+
+int gpp_evaluate_host(gpp_ctx* c, int32_t variant, int64_t nbands, int64_t ngpown, int64_t ncouls,
+                      int32_t nw, const double* wtilde, const double* i_eps,
+                      const double* aqsntemp, const double* aqsmtemp, const double* wx,
+                      int32_t wx_band_indexed, int64_t band0, int64_t band1, int32_t slabs,
+                      double* achtemp, double* asxtemp, int64_t* near_far, float* ms) {
+  int rc = comm_alive(c);
+  if (rc) return rc;
+  return comm_guard(c, gpp_evaluate_host_impl(c, variant, nbands, ngpown, ncouls, nw, wtilde,
+                                              i_eps, aqsntemp, aqsmtemp, wx, wx_band_indexed,
+                                              band0, band1, slabs, achtemp, asxtemp, near_far,
+                                              ms));
+}
+
+int gpp_run(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp, int64_t* near_far,
+            float* kernel_ms) {
+  int rc = comm_alive(c);
+  if (rc) return rc;
+  return comm_guard(c, gpp_run_impl(c, variant, achtemp, asxtemp, near_far, kernel_ms));
+}
+
+int gpp_time(gpp_ctx* c, int32_t variant, int32_t iters, float* total_ms, float* main_ms) {
+  int rc = comm_alive(c);
+  if (rc) return rc;
+  return comm_guard(c, gpp_time_impl(c, variant, iters, total_ms, main_ms));
+}
+
+int gpp_synth(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw,
+              const uint64_t* pcg_state, const double* wx, int64_t band0, int64_t band1) {
+  int rc = comm_alive(c);
+  if (rc) return rc;
+  return comm_guard(c, gpp_synth_impl(c, nbands, ngpown, ncouls, nw, pcg_state, wx, band0, band1));
+}
+
+int gpp_run_factored(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp,
+                     int64_t* near_far, float* ms) {
+  int rc = comm_alive(c);
+  if (rc) return rc;
+  return comm_guard(c, gpp_run_factored_impl(c, variant, achtemp, asxtemp, near_far, ms));
+}
+
+static int group_guard(gpp_ctx** ctxs, int n, int rc) {
+  for (int i = 0; rc != GPP_OK && ctxs && i < n; ++i) comm_guard(ctxs[i], rc);
+  return rc;
+}
+
+int gpp_run_group(gpp_ctx** ctxs, int n, int32_t variant, double* achtemp, double* asxtemp,
+                  int64_t* near_far, float* kernel_ms) {
+  for (int i = 0; ctxs && i < n; ++i) {
+    int rc = comm_alive(ctxs[i]);
+    if (rc) return rc;
+  }
+  return group_guard(ctxs, n,
+                     gpp_run_group_impl(ctxs, n, variant, achtemp, asxtemp, near_far, kernel_ms));
+}
+
+// Device-resident timing of the single-process group: `iters`
+// evaluations enqueued back to back on every device, each followed by one
+// grouped ncclAllReduce of the partials, no host synchronisation in between;
+// total_ms / main_ms = the slowest device's event time of the whole run / of
+// its summed main-kernel spans.
+static int gpp_time_group_impl(gpp_ctx** ctxs, int n, int32_t variant, int32_t iters,
+                               float* total_ms, float* main_ms) {
+  if (!ctxs || n < 1) return fail(GPP_ERR_ARG, "need at least one context");
+  CtxLock lock(ctxs, n);
+  int rc = check_variant(variant);
+  if (rc) return rc;
+  if (iters < 1) return fail(GPP_ERR_ARG, "iters must be at least 1");
+  for (int i = 0; i < n; ++i) {
+    if (!ctxs[i] || !ctxs[i]->have_problem)
+      return fail(GPP_ERR_ARG, "context " + std::to_string(i) + " has no problem uploaded");
+    if (ctxs[i]->nw != ctxs[0]->nw)
+      return fail(GPP_ERR_ARG, "contexts hold problems with different nw");
+    if (n > 1 && (!ctxs[i]->comm || ctxs[i]->nranks != n))
+      return fail(GPP_ERR_ARG, "contexts need gpp_comm_init_all over the same group");
+  }
+  std::vector<std::vector<cudaEvent_t>> evs(n, std::vector<cudaEvent_t>(2 * static_cast<size_t>(iters)));
+  int result = GPP_OK;
+  for (int i = 0; i < n && result == GPP_OK; ++i) {
+    DeviceGuard g(ctxs[i]->device);
+    for (auto& e : evs[i])
+      if (result == GPP_OK && cudaEventCreate(&e) != cudaSuccess) result = fail(GPP_ERR_CUDA, "cudaEventCreate");
+  }
+  for (int i = 0; i < n && result == GPP_OK; ++i) {
+    DeviceGuard g(ctxs[i]->device);
+    if (cudaEventRecord(ctxs[i]->ev[2], ctxs[i]->stream) != cudaSuccess)
+      result = fail(GPP_ERR_CUDA, "cudaEventRecord");
+  }
+  for (int it = 0; it < iters && result == GPP_OK; ++it) {
+    for (int i = 0; i < n && result == GPP_OK; ++i) {
+      DeviceGuard g(ctxs[i]->device);
+      result = enqueue_eval(ctxs[i], variant, false, &evs[i][2 * static_cast<size_t>(it)], false);
+    }
+    if (result == GPP_OK && n > 1) {
+      ncclResult_t r = ncclGroupStart();
+      for (int i = 0; i < n && r == ncclSuccess; ++i) {
+        gpp_ctx* c = ctxs[i];
+        r = ncclAllReduce(c->out.ptr, c->out.ptr, 4 * c->nw, ncclDouble, ncclSum, c->comm, c->stream);
+        if (r == ncclSuccess)
+          r = ncclAllReduce(c->counts.ptr, c->counts.ptr, 2, ncclUint64, ncclSum, c->comm, c->stream);
+      }
+      const ncclResult_t r2 = ncclGroupEnd();
+      if (r != ncclSuccess || r2 != ncclSuccess)
+        result = fail(GPP_ERR_NCCL, std::string("grouped ncclAllReduce: ") +
+                                        ncclGetErrorString(r != ncclSuccess ? r : r2));
+    }
+  }
+  float worst_tot = 0.f, worst_main = 0.f;
+  for (int i = 0; i < n && result == GPP_OK; ++i) {
+    gpp_ctx* c = ctxs[i];
+    DeviceGuard g(c->device);
+    if (cudaEventRecord(c->ev[3], c->stream) != cudaSuccess) {
+      result = fail(GPP_ERR_CUDA, "cudaEventRecord");
+      break;
+    }
+    result = wait_stream(c, c->stream);
+    if (result) break;
+    float tot = 0.f, mm = 0.f;
+    cudaEventElapsedTime(&tot, c->ev[2], c->ev[3]);
+    for (int it = 0; it < iters; ++it) {
+      float x = 0.f;
+      cudaEventElapsedTime(&x, evs[i][2 * it], evs[i][2 * it + 1]);
+      mm += x;
+    }
+    worst_tot = std::max(worst_tot, tot);
+    worst_main = std::max(worst_main, mm);
+  }
+  for (int i = 0; i < n; ++i) {
+    DeviceGuard g(ctxs[i]->device);
+    for (auto& e : evs[i])
+      if (e) cudaEventDestroy(e);
+  }
+  if (result == GPP_OK) {
+    if (total_ms) *total_ms = worst_tot;
+    if (main_ms) *main_ms = worst_main;
+  }
+  return result;
+}
+
+int gpp_time_group(gpp_ctx** ctxs, int n, int32_t variant, int32_t iters, float* total_ms,
+                   float* main_ms) {
+  for (int i = 0; ctxs && i < n; ++i) {
+    int rc = comm_alive(ctxs[i]);
+    if (rc) return rc;
+  }
+  return group_guard(ctxs, n, gpp_time_group_impl(ctxs, n, variant, iters, total_ms, main_ms));
 }
 
 }  // extern "C"

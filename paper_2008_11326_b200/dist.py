@@ -82,6 +82,16 @@ class ShardedGPP:
         """Evaluate this rank's shard; the result is the all-rank total."""
         return self.ctx.run(variant, counts=counts)
 
+    def evaluate(self, problem, variant: str = "rcp_sq", counts: bool = False):
+        """End to end from host arrays: this rank uploads its band shard of
+        aqsntemp / aqsmtemp and 1/N of the igp columns of wtilde / i_eps, the
+        columns are broadcast over NVLink, the shard is evaluated pipelined
+        with its upload, and the partials are all-reduced (gpp_evaluate_host
+        with the communicator attached): (total GPPResult, (near, far) | None,
+        device ms)."""
+        return self.ctx.evaluate_host(problem, variant, band_range=self.band_range(int(problem.nbands)),
+                                      counts=counts)
+
     def close(self) -> None:
         self.ctx.close()
 
@@ -109,6 +119,54 @@ class MultiDeviceGPP:
         n = len(self.ctxs)
         for rank, ctx in enumerate(self.ctxs):
             ctx.upload(problem, band_range(int(problem.nbands), n, rank), force=force)
+
+    def synth(self, nbands: int, ngpown: int, ncouls: int, seed: int = 42, nw: int = 2) -> None:
+        """Draw every device's band shard of synth_problem on that device."""
+        n = len(self.ctxs)
+        for rank, ctx in enumerate(self.ctxs):
+            ctx.synth(nbands, ngpown, ncouls, seed=seed, nw=nw,
+                      band_range=band_range(nbands, n, rank))
+
+    def time(self, variant: str = "rcp_sq", iters: int = 10) -> tuple[float, float]:
+        """Device-resident timing of ``iters`` group evaluations (each with its
+        grouped allreduce, no host sync in between; gpp_time_group):
+        (slowest device total ms, slowest device summed main-kernel ms)."""
+        import ctypes
+
+        from . import _lib
+        from .kernel import _variant_code
+
+        tot, main = ctypes.c_float(), ctypes.c_float()
+        _lib.check(self._lib.gpp_time_group(self._arr, len(self.ctxs), _variant_code(variant), int(iters),
+                                            ctypes.byref(tot), ctypes.byref(main)), "gpp_time_group")
+        return float(tot.value), float(main.value)
+
+    def evaluate(self, problem, variant: str = "rcp_sq"):
+        """End to end from host arrays on every device at once: one thread per
+        device runs gpp_evaluate_host on its band shard (column-split
+        wtilde / i_eps upload + NCCL broadcast, allreduce of the partials).
+        Returns (total GPPResult, slowest device ms)."""
+        import threading
+
+        n = len(self.ctxs)
+        out: list = [None] * n
+        errs: list = []
+
+        def work(rank):
+            try:
+                out[rank] = self.ctxs[rank].evaluate_host(
+                    problem, variant, band_range=band_range(int(problem.nbands), n, rank))
+            except Exception as e:  # noqa: BLE001 -- re-raised below
+                errs.append(e)
+
+        ts = [threading.Thread(target=work, args=(r,)) for r in range(n)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        if errs:
+            raise errs[0]
+        return out[0][0], max(o[2] for o in out)
 
     def run(self, variant: str = "rcp_sq", counts: bool = True):
         """(GPPResult, (near, far) | None, slowest-device kernel ms) of the whole problem."""

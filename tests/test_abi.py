@@ -74,9 +74,10 @@ def test_argument_validation_without_gpu():
         assert lib.gpp_upload(h, 1, 1, 1, 0, p, p, p, p, p, 0, 0, 1) == _lib.GPP_ERR_ARG
         # null pointer
         assert lib.gpp_upload(h, 1, 1, 1, 2, None, p, p, p, p, 0, 0, 1) == _lib.GPP_ERR_ARG
-        # band range
-        assert lib.gpp_upload(h, 4, 1, 1, 2, p, p, p, p, p, 0, 3, 3) == _lib.GPP_ERR_ARG
+        # band range (an empty shard [3, 3) is valid: more ranks than bands)
+        assert lib.gpp_upload(h, 4, 1, 1, 2, p, p, p, p, p, 0, 3, 2) == _lib.GPP_ERR_ARG
         assert lib.gpp_upload(h, 4, 1, 1, 2, p, p, p, p, p, 0, 0, 5) == _lib.GPP_ERR_ARG
+        assert lib.gpp_upload(h, 4, 1, 1, 2, p, p, p, p, p, 0, -1, 2) == _lib.GPP_ERR_ARG
         # run before upload / bad variant
         out = np.zeros(4)
         assert lib.gpp_run(h, 2, _lib.dptr(out), _lib.dptr(out), None, None) == _lib.GPP_ERR_ARG

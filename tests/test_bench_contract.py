@@ -21,6 +21,9 @@ def test_reference_arm_prints_contract_line():
     assert KEYS <= set(d), KEYS - set(d)
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "TFLOP/s"
     assert d["higher_is_better"] is True and d["n_gpus"] == 1
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    # the unmodified reference when baseline/_ref holds it, else the oracle port
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["cpu_model"] and d["cpu_baseline"]["OPENBLAS_NUM_THREADS"]
+    assert d["numerator"]["flops_per_step"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["config"]["workload"].startswith("paper")

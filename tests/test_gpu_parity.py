@@ -566,3 +566,101 @@ def test_shared_context_serialises_callers():
     finally:
         ctx.close()
     assert bad == []
+
+
+def test_empty_band_shard_contributes_zeros():
+    """More ranks than bands: a rank's shard [b, b) is empty -- it uploads
+    nothing, contributes zeros and still joins the collective (no rank can
+    fail before the allreduce while its peers wait in it)."""
+    p = synth_problem(6, 5, 700, seed=2, nw=3, check=False)
+    whole = evaluate_variant(p, "rcp_sq")
+    ctx = GPPContext(0)
+    try:
+        ctx.upload(p, (3, 3))
+        r, (near, far), _ = ctx.run("rcp_sq", counts=True)
+        assert not np.any(r.achtemp) and not np.any(r.asxtemp) and near == far == 0
+        r2 = ctx.evaluate_host(p, "rcp_sq", band_range=(6, 6), counts=True)
+        assert not np.any(r2[0].achtemp) and r2[1] == (0, 0)
+        tot, main = ctx.time("rcp_sq", 3)
+        assert tot >= 0.0
+        parts = []
+        for br in ((0, 3), (3, 3), (3, 6)):
+            ctx.upload(p, br, force=True)
+            parts.append(ctx.run("rcp_sq", counts=False)[0])
+    finally:
+        ctx.close()
+    ach = sum(x.achtemp for x in parts)
+    asx = sum(x.asxtemp for x in parts)
+    assert max_rel_error(type(whole)(achtemp=ach, asxtemp=asx), whole) <= 1e-13
+
+
+def test_group_path_bitmatches_single_context():
+    """The single-process multi-device path (MultiDeviceGPP: gpp_comm_init_all,
+    gpp_run_group, gpp_time_group, threaded evaluate) on one device gives the
+    bits of the plain context; its timing entry point runs."""
+    from paper_2008_11326_b200.dist import MultiDeviceGPP
+
+    dims = (512, 66, 32768)
+    ctx = GPPContext(0)
+    try:
+        ctx.synth(*dims, seed=1, nw=3)
+        want = ctx.run("rcp_sq", counts=False)[0]
+    finally:
+        ctx.close()
+    g = MultiDeviceGPP([0])
+    try:
+        g.synth(*dims, seed=1, nw=3)
+        got, (near, far), _ = g.run("rcp_sq", counts=True)
+        fast = g.run("rcp_sq", counts=False)[0]
+        assert _bits_equal(fast, want)
+        tot, main = g.time("rcp_sq", 3)
+        assert tot > 0.0 and 0.0 < main <= tot
+        p = synth_problem(*dims, seed=1, nw=3, check=False)
+        e2e, _ = g.evaluate(p, "rcp_sq")
+        assert _bits_equal(e2e, want)
+    finally:
+        g.close()
+
+
+def test_pinned_pageable_and_column_split_uploads_bitwise():
+    """Every upload route gives the same bits: pageable arrays (library
+    staging ring), page-locked arrays (direct DMA), and the column-split
+    wtilde / i_eps upload the band-sharded e2e path uses (forced on one rank
+    with GPP_COLUMN_UPLOAD=1, in a subprocess)."""
+    import subprocess
+    import sys
+
+    from paper_2008_11326_b200._lib import check, load
+
+    p = synth_problem(300, 13, 9000, seed=4, nw=3, check=False)
+    want = evaluate_variant(p, "rcp_sq")
+    q = GPPProblem(p.nbands, p.ngpown, p.ncouls, p.wtilde.copy(order="F"), p.i_eps.copy(order="F"),
+                   p.aqsntemp.copy(order="F"), p.aqsmtemp.copy(order="F"), p.wx.copy())
+    assert _bits_equal(evaluate_variant(q, "rcp_sq"), want)  # pageable (writeable: re-uploaded)
+    lib = load()
+    arrs = [q.wtilde, q.i_eps, q.aqsntemp, q.aqsmtemp]
+    for a in arrs:
+        check(lib.gpp_host_register(a.ctypes.data, a.nbytes))
+    try:
+        assert _bits_equal(evaluate_variant(q, "rcp_sq"), want)  # pinned
+    finally:
+        for a in arrs:
+            lib.gpp_host_unregister(a.ctypes.data)
+    code = (
+        "import json\n"
+        "from paper_2008_11326_b200 import GPPContext, synth_problem\n"
+        "p = synth_problem(300, 13, 9000, seed=4, nw=3, check=False)\n"
+        "c = GPPContext(0)\n"
+        "r = [c.evaluate_host(p, 'rcp_sq', band_range=br)[0] for br in (None, (0, 140), (140, 300))]\n"
+        "f = lambda z: [[v.real, v.imag] for v in z]\n"
+        "print(json.dumps([f(r[0].achtemp), f(r[0].asxtemp), f(r[1].achtemp + r[2].achtemp)]))\n"
+    )
+    import json
+    import os
+
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         env={**os.environ, "GPP_COLUMN_UPLOAD": "1"}, cwd=str(__import__("conftest").ROOT))
+    assert out.returncode == 0, out.stderr[-2000:]
+    ach, asx, shards = (as_complex(x) for x in json.loads(out.stdout.strip().splitlines()[-1]))
+    assert np.array_equal(ach, want.achtemp) and np.array_equal(asx, want.asxtemp)
+    assert max_rel_error(type(want)(achtemp=shards, asxtemp=want.asxtemp), want) <= 1e-12
