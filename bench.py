@@ -353,10 +353,17 @@ def ncu_capture(args, timeout_s: float = 420.0) -> dict | None:
         return {"error": f"ncu failed: {e}"}
     if proc.returncode != 0 or not out.exists():
         return {"error": f"ncu rc={proc.returncode}: {(proc.stderr or proc.stdout)[-300:]}"}
-    rows = list(csv.reader(io.StringIO(out.read_text())))
-    out.unlink(missing_ok=True)
-    hdr = rows[0]
-    data = [r for r in rows[2:] if len(r) == len(hdr)]
+    text = out.read_text()
+    if not os.environ.get("GPP_NCU_KEEP"):
+        out.unlink(missing_ok=True)
+    # The log also holds ncu's own "==PROF==" lines: the table starts at the
+    # header row ("ID", ...), then one row of units, then one row per launch.
+    rows = [r for r in csv.reader(io.StringIO(text)) if r]
+    start = next((i for i, r in enumerate(rows) if r[0] == "ID"), None)
+    if start is None:
+        return {"error": f"ncu produced no table: {text[-300:]}"}
+    hdr = rows[start]
+    data = [r for r in rows[start + 2:] if len(r) == len(hdr) and r[0].isdigit()]
     col = {k: i for i, k in enumerate(hdr)}
 
     def val(r, k):
