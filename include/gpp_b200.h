@@ -154,10 +154,11 @@ int gpp_evaluate_host(gpp_ctx* ctx, int32_t variant, int64_t nbands, int64_t ngp
                       int32_t wx_band_indexed, int64_t band0, int64_t band1, int32_t slabs,
                       double* achtemp, double* asxtemp, int64_t* near_far, float* ms);
 
-/* ZGEMM-factored evaluation of the uploaded problem: the reference's own
- * production algorithm (rooflab/gpp/kernel.py:98-114) -- one ZGEMM forms
- * W = aqsntemp conj(aqsmtemp)^T (cuBLAS), then the variant's branch terms
- * per (iw, ig, igp) are contracted with W.  Only valid for a band-invariant
+/* Factored evaluation of the uploaded problem: the reference's own
+ * production algorithm (rooflab/gpp/kernel.py:98-114) -- the band sum
+ * W = aqsntemp conj(aqsmtemp)^T and the contraction of the variant's branch
+ * terms per (iw, ig, igp) with W, fused in one hand-written FP64 kernel
+ * (gpp_factored_kernel; W stays in registers).  Only valid for a band-invariant
  * wx (GPP_ERR_ARG otherwise).  A different algorithm from the per-instance
  * nest gpp_run evaluates: time to solution, not a roofline figure.  With a
  * communicator attached the partials are all-reduced as in gpp_run. */

@@ -1264,38 +1264,119 @@ __global__ void __launch_bounds__(256) gpp_slot_finalize_kernel(
   }
 }
 
-// ZGEMM-factored evaluation (the reference's production algorithm,
+// Factored evaluation (the reference's production algorithm,
 // rooflab/gpp/kernel.py:98-114), valid when wx does not depend on the band:
-// W[ig, igp] = sum_band aqsntemp[ig, band] conj(aqsmtemp[igp, band]) comes
-// from one ZGEMM (cuBLAS, FP64 tensor cores); this kernel forms the branch
-// terms of variant V per (iw, ig, igp) exactly as the reference's
-// variant_terms does (PlainPolicy<V>, kernel.py:63-95) and contracts them with
-// W.  A different algorithm from the per-instance nest -- time to solution,
-// never a roofline figure.  Counts are scaled by nb, the
-// band count W summed over (kernel.py:130-137).
+// the band sum is factored out of the branch terms,
+//     W[ig, igp] = sum_band aqsntemp[ig, band] conj(aqsmtemp[igp, band])
+// (kernel.py:108), then ach[iw] = sum sch[iw, ig, igp] W, asx likewise.
+// One fused kernel: an item is (256-ig block, kFacIgp-igp tile); thread <->
+// ig accumulates its kFacIgp complex W entries over all bands in registers
+// (aqsntemp streamed with a register prefetch ring, the aqsmtemp tile staged
+// in shared memory and read as warp-uniform broadcasts: 4 DFMA per complex
+// multiply-add, FP64 vector pipe), then forms variant V's branch terms per
+// (iw, ig, igp) exactly as PlainPolicy<V> does (kernel.py:63-95) and
+// contracts them with W -- W never goes to memory.  A different algorithm
+// from the per-instance nest (it exploits the band invariance of the
+// reference's wx): time to solution, never a roofline figure.
+// Counts are scaled by nb, the band count W summed over (kernel.py:130-137).
+constexpr int kFacIgp = 8;      // igp per item
+constexpr int kFacChunk = 64;   // aqsmtemp bands staged per pass
+constexpr int kFacDepth = 4;    // aqsntemp bands in flight per thread
+
 template <int V, int NW>
-__global__ void __launch_bounds__(kThreads) gpp_factored_terms_kernel(
-    const double2* __restrict__ W, const double2* __restrict__ wtilde,
-    const double2* __restrict__ eps, const double* __restrict__ wx0, int nw_total, int iw0,
-    long long n_elems, unsigned long long nb, double* partials, unsigned long long* cpartials) {
+__global__ void __launch_bounds__(kThreads, 2) gpp_factored_kernel(
+    const double2* __restrict__ aqsn, const double2* __restrict__ aqsm,
+    const double2* __restrict__ wtilde, const double2* __restrict__ eps,
+    const double* __restrict__ wx0, int nw_total, int iw0, int ncouls, int ngpown, int nbands,
+    int n_igptile, long long n_items, unsigned long long nb_scale, double* partials,
+    unsigned long long* cpartials) {
+  __shared__ double2 s_am[kFacChunk][kFacIgp];
+  // This thread's ach / asx partials across its items (shared memory, so the
+  // registers stay with the W accumulators).
+  __shared__ double s_acc[4 * NW][kThreads];
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < 4 * NW; ++k) s_acc[k][tid] = 0.0;
+  unsigned n_near = 0, n_far = 0;
+  const size_t nc = static_cast<size_t>(ncouls);
+  for (long long item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int igpt = static_cast<int>(item % n_igptile);
+    const int igb = static_cast<int>(item / n_igptile);
+    const int ig = igb * kThreads + tid;
+    const bool vig = ig < ncouls;
+    const int igc = vig ? ig : ncouls - 1;
+    double2 W[kFacIgp];
+#pragma unroll
+    for (int j = 0; j < kFacIgp; ++j) W[j] = make_double2(0.0, 0.0);
+    const double2* ap = aqsn + igc;
+    for (int b0 = 0; b0 < nbands; b0 += kFacChunk) {
+      const int nb = min(kFacChunk, nbands - b0);
+      __syncthreads();  // the previous pass's reads of s_am are done
+      for (int k = tid; k < nb * kFacIgp; k += kThreads) {
+        const int bb = k / kFacIgp, j = k - bb * kFacIgp;
+        const int igp = igpt * kFacIgp + j;
+        s_am[bb][j] = igp < ngpown ? __ldg(aqsm + static_cast<size_t>(b0 + bb) * ngpown + igp)
+                                   : make_double2(0.0, 0.0);
+      }
+      __syncthreads();
+      double2 ring[kFacDepth];
+#pragma unroll
+      for (int s = 0; s < kFacDepth; ++s)
+        ring[s] = s < nb ? __ldg(ap + static_cast<size_t>(b0 + s) * nc) : make_double2(0.0, 0.0);
+      for (int bb = 0; bb < nb; bb += kFacDepth) {
+#pragma unroll
+        for (int s = 0; s < kFacDepth; ++s) {
+          const double2 an = ring[s];
+          if (bb + s + kFacDepth < nb) ring[s] = __ldg(ap + static_cast<size_t>(b0 + bb + s + kFacDepth) * nc);
+          if (bb + s < nb) {
+#pragma unroll
+            for (int j = 0; j < kFacIgp; ++j) {
+              const double2 am = s_am[bb + s][j];
+              W[j].x = fma(an.x, am.x, fma(an.y, am.y, W[j].x));   // an * conj(am)
+              W[j].y = fma(an.y, am.x, fma(-an.x, am.y, W[j].y));
+            }
+          }
+        }
+      }
+    }
+    Acc<NW> acc;
+#pragma unroll
+    for (int iw = 0; iw < NW; ++iw) {
+      acc.a[iw] = make_double2(s_acc[4 * iw + 0][tid], s_acc[4 * iw + 1][tid]);
+      acc.b[iw] = make_double2(s_acc[4 * iw + 2][tid], s_acc[4 * iw + 3][tid]);
+    }
+    acc.nn = n_near;
+    acc.nf = n_far;
+    double wx[NW];
+#pragma unroll
+    for (int iw = 0; iw < NW; ++iw) wx[iw] = __ldg(wx0 + iw0 + iw);
+#pragma unroll
+    for (int j = 0; j < kFacIgp; ++j) {
+      const int igp = igpt * kFacIgp + j;
+      const bool v = vig && igp < ngpown;
+      const size_t off = static_cast<size_t>(min(igp, ngpown - 1)) * nc + igc;
+      const typename PlainPolicy<V>::St st = PlainPolicy<V>::make(__ldg(wtilde + off), __ldg(eps + off), v);
+      PlainPolicy<V>::template tuple<NW, true, false>(st, W[j].x, W[j].y, wx, acc);
+    }
+#pragma unroll
+    for (int iw = 0; iw < NW; ++iw) {
+      s_acc[4 * iw + 0][tid] = acc.a[iw].x;
+      s_acc[4 * iw + 1][tid] = acc.a[iw].y;
+      s_acc[4 * iw + 2][tid] = acc.b[iw].x;
+      s_acc[4 * iw + 3][tid] = acc.b[iw].y;
+    }
+    n_near = acc.nn;
+    n_far = acc.nf;
+  }
   Acc<NW> acc;
 #pragma unroll
   for (int iw = 0; iw < NW; ++iw) {
-    acc.a[iw] = make_double2(0.0, 0.0);
-    acc.b[iw] = make_double2(0.0, 0.0);
+    acc.a[iw] = make_double2(s_acc[4 * iw + 0][tid], s_acc[4 * iw + 1][tid]);
+    acc.b[iw] = make_double2(s_acc[4 * iw + 2][tid], s_acc[4 * iw + 3][tid]);
   }
-  acc.nn = 0;
-  acc.nf = 0;
-  double wx[NW];
-#pragma unroll
-  for (int iw = 0; iw < NW; ++iw) wx[iw] = __ldg(wx0 + iw0 + iw);
-  for (long long e = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x; e < n_elems;
-       e += static_cast<long long>(gridDim.x) * kThreads) {
-    const typename PlainPolicy<V>::St st = PlainPolicy<V>::make(__ldg(wtilde + e), __ldg(eps + e), true);
-    const double2 w = __ldg(W + e);
-    PlainPolicy<V>::template tuple<NW, true, false>(st, w.x, w.y, wx, acc);
-  }
-  block_reduce_write<NW, true>(acc, partials, cpartials, nb);
+  acc.nn = n_near;
+  acc.nf = n_far;
+  block_reduce_write<NW, true>(acc, partials, cpartials, nb_scale);
 }
 
 // ---------------------------------------------------------------------------

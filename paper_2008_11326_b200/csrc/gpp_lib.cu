@@ -1,7 +1,6 @@
 // gpp_lib.cu -- host side of libgpp_b200.so: the C ABI declared in
 // include/gpp_b200.h, the device-buffer manager, launch planning, the NCCL
 // band-shard combine and the FP64 peak microbenchmark.
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <omp.h>
@@ -175,10 +174,8 @@ struct gpp_ctx {
   DevBuf<unsigned> ticket;   // slot finalize: last-block ticket (self-resetting)
   std::mutex mu;             // one caller at a time (the ABI's contexts are shareable)
 
-  // ZGEMM-factored path (gpp_run_factored).
+  // Factored path (gpp_run_factored): needs a band-invariant wx.
   bool wx_band_invariant = false;
-  cublasHandle_t blas = nullptr;
-  DevBuf<double2> weight;  // (ncouls, ngpown) F-order
 };
 
 namespace {
@@ -937,8 +934,6 @@ void gpp_destroy(gpp_ctx* c) {
     if (c->kstream2) cudaStreamSynchronize(c->kstream2);
     if (c->nstream) cudaStreamSynchronize(c->nstream);
     if (c->comm) ncclCommDestroy(c->comm);
-    if (c->blas) cublasDestroy(c->blas);
-    c->weight.release();
     c->wtilde.release();
     c->eps.release();
     c->aqsn.release();
@@ -1659,7 +1654,7 @@ static int gpp_synth_impl(gpp_ctx* c, int64_t nbands, int64_t ngpown, int64_t nc
 }
 
 static int gpp_run_factored_impl(gpp_ctx* c, int32_t variant, double* achtemp, double* asxtemp,
-                     int64_t* near_far, float* ms) {
+                                 int64_t* near_far, float* ms) {
   CtxLock lock(c);
   if (!c) return fail(GPP_ERR_ARG, "ctx is NULL");
   if (variant < GPP_VARIANT_DIV || variant > GPP_VARIANT_RCP_SQ)
@@ -1670,60 +1665,58 @@ static int gpp_run_factored_impl(gpp_ctx* c, int32_t variant, double* achtemp, d
     return fail(GPP_ERR_ARG, "the factored path needs a band-invariant wx (the reference's (nw,) vector)");
   DeviceGuard g(c->device);
   if (!g.ok) return cuda_fail(g.err, "cudaSetDevice");
-  if (!c->blas) {
-    if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) return fail(GPP_ERR_CUDA, "cublasCreate failed");
-  }
-  if (cublasSetStream(c->blas, c->stream) != CUBLAS_STATUS_SUCCESS)
-    return fail(GPP_ERR_CUDA, "cublasSetStream failed");
-  const size_t n_el = static_cast<size_t>(c->ncouls) * c->ngpown;
-  GPP_CUDA(c->weight.ensure(n_el));
   GPP_CUDA(cudaEventRecord(c->ev[2], c->stream));
-  // W = aqsn (nc x nb) * conj(aqsm)^T (nb x ng): one ZGEMM.
-  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
-  const cublasStatus_t st = cublasZgemm(
-      c->blas, CUBLAS_OP_N, CUBLAS_OP_C, static_cast<int>(c->ncouls), static_cast<int>(c->ngpown),
-      static_cast<int>(c->nbands), &one, reinterpret_cast<const cuDoubleComplex*>(c->aqsn.ptr),
-      static_cast<int>(c->ncouls), reinterpret_cast<const cuDoubleComplex*>(c->aqsm.ptr),
-      static_cast<int>(c->ngpown), &zero, reinterpret_cast<cuDoubleComplex*>(c->weight.ptr),
-      static_cast<int>(c->ncouls));
-  if (st != CUBLAS_STATUS_SUCCESS) return fail(GPP_ERR_CUDA, "cublasZgemm failed");
-  std::vector<std::pair<int, int>> groups;
-  nw_groups(c->nw, gpp::kMaxNwGroup, &groups);
-  const int grid = std::max(1, std::min<int>(c->num_sms * 4, static_cast<int>(
-                                   (n_el + gpp::kThreads - 1) / gpp::kThreads)));
-  GPP_CUDA(c->partials.ensure(static_cast<size_t>(grid) * 4 * gpp::kMaxNwGroup));
-  GPP_CUDA(c->cpartials.ensure(static_cast<size_t>(grid) * 2));
-  bool first = true;
-  for (const auto& gr : groups) {
-    const int iw0 = gr.first, nwg = gr.second;
-#define GPP_FAC(V, NWC)                                                                          \
-  gpp::gpp_factored_terms_kernel<V, NWC><<<grid, gpp::kThreads, 0, c->stream>>>(                 \
-      c->weight.ptr, c->wtilde.ptr, c->eps.ptr, c->wxb.ptr, c->nw, iw0,                          \
-      static_cast<long long>(n_el), static_cast<unsigned long long>(c->nbands), c->partials.ptr, \
-      c->cpartials.ptr)
-#define GPP_FAC_NW(V)              \
-  switch (nwg) {                   \
-    case 1: GPP_FAC(V, 1); break;  \
-    case 2: GPP_FAC(V, 2); break;  \
-    case 3: GPP_FAC(V, 3); break;  \
-    default: GPP_FAC(V, 4); break; \
+  if (c->nbands == 0) {
+    int rc = enqueue_eval(c, GPP_VARIANT_RCP_SQ, near_far != nullptr, nullptr, false);
+    if (rc) return rc;
+  } else {
+    std::vector<std::pair<int, int>> groups;
+    nw_groups(c->nw, gpp::kMaxNwGroup, &groups);
+    const int n_igblk = static_cast<int>((c->ncouls + gpp::kThreads - 1) / gpp::kThreads);
+    const int n_igptile = static_cast<int>((c->ngpown + gpp::kFacIgp - 1) / gpp::kFacIgp);
+    const long long n_items = static_cast<long long>(n_igblk) * n_igptile;
+    bool first = true;
+    for (const auto& gr : groups) {
+      const int iw0 = gr.first, nwg = gr.second;
+      using FacFn = void (*)(const double2*, const double2*, const double2*, const double2*,
+                             const double*, int, int, int, int, int, int, long long,
+                             unsigned long long, double*, unsigned long long*);
+      FacFn fn = nullptr;
+#define GPP_FAC_NW(V)                                               \
+  switch (nwg) {                                                    \
+    case 1: fn = gpp::gpp_factored_kernel<V, 1>; break;             \
+    case 2: fn = gpp::gpp_factored_kernel<V, 2>; break;             \
+    case 3: fn = gpp::gpp_factored_kernel<V, 3>; break;             \
+    default: fn = gpp::gpp_factored_kernel<V, 4>; break;            \
   }
-    if (variant == GPP_VARIANT_DIV) {
-      GPP_FAC_NW(0)
-    } else if (variant == GPP_VARIANT_RCP) {
-      GPP_FAC_NW(1)
-    } else {
-      GPP_FAC_NW(2)
-    }
+      if (variant == GPP_VARIANT_DIV) {
+        GPP_FAC_NW(0)
+      } else if (variant == GPP_VARIANT_RCP) {
+        GPP_FAC_NW(1)
+      } else {
+        GPP_FAC_NW(2)
+      }
 #undef GPP_FAC_NW
-#undef GPP_FAC
-    GPP_CUDA(cudaGetLastError());
-    c->launches += 2;  // branch terms + finalize
-    pick_finalize(nwg)<<<1, 256, 0, c->stream>>>(c->partials.ptr, c->cpartials.ptr, grid, c->nw,
-                                                  iw0, 0, first ? 1 : 0, 1, c->out.ptr,
-                                                  c->counts.ptr);
-    GPP_CUDA(cudaGetLastError());
-    first = false;
+      int bps = 0;
+      GPP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, reinterpret_cast<const void*>(fn),
+                                                             gpp::kThreads, 0));
+      const int grid = static_cast<int>(std::max<long long>(
+          1, std::min<long long>(static_cast<long long>(std::max(bps, 1)) * c->num_sms, n_items)));
+      GPP_CUDA(c->partials.ensure(static_cast<size_t>(grid) * 4 * gpp::kMaxNwGroup));
+      GPP_CUDA(c->cpartials.ensure(static_cast<size_t>(grid) * 2));
+      fn<<<grid, gpp::kThreads, 0, c->stream>>>(
+          c->aqsn.ptr, c->aqsm.ptr, c->wtilde.ptr, c->eps.ptr, c->wxb.ptr, c->nw, iw0,
+          static_cast<int>(c->ncouls), static_cast<int>(c->ngpown), static_cast<int>(c->nbands),
+          n_igptile, n_items, static_cast<unsigned long long>(c->nbands), c->partials.ptr,
+          c->cpartials.ptr);
+      GPP_CUDA(cudaGetLastError());
+      c->launches += 2;  // fused GEMM + terms, finalize
+      pick_finalize(nwg)<<<1, 256, 0, c->stream>>>(c->partials.ptr, c->cpartials.ptr, grid, c->nw,
+                                                    iw0, 0, first ? 1 : 0, 1, c->out.ptr,
+                                                    c->counts.ptr);
+      GPP_CUDA(cudaGetLastError());
+      first = false;
+    }
   }
   GPP_CUDA(cudaEventRecord(c->ev[3], c->stream));
   int rc = finish_run(c, achtemp, asxtemp, near_far);

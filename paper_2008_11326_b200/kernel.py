@@ -239,7 +239,7 @@ class GPPContext:
         return result, ((int(nf[0]), int(nf[1])) if counts else None), float(ms.value)
 
     def run_factored(self, variant: str = "rcp_sq", counts: bool = True):
-        """The reference's ZGEMM-factored algorithm on the device
+        """The reference's factored algorithm on the device (one fused repo kernel)
         (gpp_run_factored): (GPPResult, (near, far) | None, device_ms).
         Band-invariant wx only; a different algorithm from run()."""
         _reference_variant(variant)
@@ -388,7 +388,7 @@ def complex_reciprocal(z):
 
 
 def evaluate_factored(problem, variant: str = "rcp_sq", device: int = 0) -> GPPResult:
-    """The reference's production algorithm (kernel.py:98-114: ZGEMM of the
+    """The reference's production algorithm (kernel.py:98-114: the GEMM of the
     band weights, then the branch terms) on the GPU.  Time-to-solution path
     for band-invariant wx; evaluate_variant runs the per-instance nest."""
     _reference_variant(variant)

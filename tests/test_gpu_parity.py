@@ -380,7 +380,7 @@ def test_single_process_group_api():
 
 @pytest.mark.parametrize("variant", ["div", "rcp", "rcp_sq"])
 def test_factored_path_vs_reference(variant):
-    """gpp_run_factored (ZGEMM + terms, the reference's own algorithm)."""
+    """gpp_run_factored (band-weight GEMM fused with the terms in one repo kernel: the reference's own algorithm)."""
     ctx = GPPContext(0)
     try:
         for case in [c for c in SMALL if c["dims"] in ([5, 3, 40], [47, 2, 33], [64, 64, 512])]:
@@ -664,3 +664,22 @@ def test_pinned_pageable_and_column_split_uploads_bitwise():
     ach, asx, shards = (as_complex(x) for x in json.loads(out.stdout.strip().splitlines()[-1]))
     assert np.array_equal(ach, want.achtemp) and np.array_equal(asx, want.asxtemp)
     assert max_rel_error(type(want)(achtemp=shards, asxtemp=want.asxtemp), want) <= 1e-12
+
+
+@pytest.mark.parametrize("dims,nw", [((24, 7, 300), 5), ((130, 17, 2000), 1), ((700, 9, 1000), 4)])
+def test_factored_kernel_odd_shapes_vs_oracle(dims, nw):
+    """The fused factored kernel at ragged igp tiles (ngpown not a multiple
+    of its 8-igp tile), band counts not a multiple of its 64-band staging,
+    and frequency groups (nw 4, 5): against the oracle's factored path."""
+    p = synth_problem(*dims, seed=3, nw=nw, check=False)
+    want = orc.evaluate_variant(p, "rcp_sq")
+    _, near, far = orc.branch_stats(p, "rcp_sq")
+    ctx = GPPContext(0)
+    try:
+        ctx.upload(p)
+        for variant in ("rcp_sq", "rcp", "div"):
+            got, nf, _ = ctx.run_factored(variant, counts=True)
+            assert max_rel_error(got, want) <= 1e-12, variant
+            assert nf == (near, far), variant
+    finally:
+        ctx.close()
