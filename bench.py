@@ -79,6 +79,8 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", choices=tuple(WORKLOADS), default="paper")
+    ap.add_argument("--dims", type=int, nargs=3, default=None, metavar=("NBANDS", "NGPOWN", "NCOULS"),
+                    help="explicit (nbands, ngpown, ncouls) instead of --workload (sweep points)")
     ap.add_argument("--nw", type=int, default=3)
     ap.add_argument("--seed", type=int, default=None,
                     help="synth_problem seed (default: 1; 42 for the weak workload, whose "
@@ -93,6 +95,11 @@ def parse_args():
     if a.seed is None:
         a.seed = 42 if a.workload == "weak" else 1
     return a
+
+
+def dims_of(args) -> tuple[int, int, int]:
+    dims = getattr(args, "dims", None)
+    return tuple(dims) if dims else WORKLOADS[args.workload]
 
 
 def lib_sha256() -> str | None:
@@ -325,7 +332,7 @@ def ncu_child(args):
     from paper_2008_11326_b200 import GPPContext
     from paper_2008_11326_b200.dist import band_range
 
-    nb, ng, nc = WORKLOADS[args.workload]
+    nb, ng, nc = dims_of(args)
     ctx = GPPContext(0)
     for r in range(args.gpus):
         ctx.synth(nb, ng, nc, seed=args.seed, nw=args.nw, band_range=band_range(nb, args.gpus, r))
@@ -343,7 +350,7 @@ def ncu_capture(args, timeout_s: float = 420.0) -> dict | None:
            "--page", "raw", "--csv", "--print-units", "base", "--log-file", str(out),
            sys.executable, str(ROOT / "bench.py"), "--ncu-child", "--workload", args.workload,
            "--nw", str(args.nw), "--seed", str(args.seed), "--variant", args.variant,
-           "--gpus", str(args.gpus)]
+           "--gpus", str(args.gpus), "--dims", *map(str, dims_of(args))]
     env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
     env["CUDA_VISIBLE_DEVICES"] = env.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0]
     t0 = time.perf_counter()
@@ -496,7 +503,7 @@ def run_ours(args, dist: Dist):
     from paper_2008_11326_b200.counters import BranchStats, algorithmic_flops, counters_from_stats, fma_ratio
     from paper_2008_11326_b200.dist import MultiDeviceGPP, ShardedGPP, band_range
 
-    dims = WORKLOADS[args.workload]
+    dims = dims_of(args)
     nb, ng, nc = dims
     device = dist.local_rank
     load()
