@@ -1202,11 +1202,23 @@ bool column_split(const gpp_ctx* c) {
     const char* e = std::getenv("GPP_COLUMN_UPLOAD");
     return e && e[0] == '1';
   }();
-  return (c->comm && c->nranks > 1) || force;
+  return (c->comm && c->nranks > 1) || force || std::getenv("GPP_COLUMN_SIM") != nullptr;
+}
+
+// GPP_COLUMN_SIM=N (timing projection only, tools/probe_shard_e2e.py): on a
+// single rank, upload just rank 0's 1/N of the columns and skip the
+// broadcasts -- the H2D and compute of one rank of N; the result is wrong.
+int column_sim() {
+  static const int n = [] {
+    const char* e = std::getenv("GPP_COLUMN_SIM");
+    return e ? std::max(1, std::atoi(e)) : 1;
+  }();
+  return n;
 }
 
 int upload_we_split(gpp_ctx* c, const HostProblem& h, const HostPins& pins) {
-  const int n = (c->comm && c->nranks > 1) ? c->nranks : 1, me = n > 1 ? c->rank : 0;
+  const bool real = c->comm && c->nranks > 1;
+  const int n = real ? c->nranks : column_sim(), me = real ? c->rank : 0;
   auto g0 = [&](int r) { return h.ngpown * r / n; };
   const int64_t a = g0(me), b = g0(me + 1), nc = h.ncouls;
   int rc = copy_cols(c, c->wtilde.ptr + a * nc, h.wtilde + 2 * a * nc, nc, b - a, 0, nc,
@@ -1216,7 +1228,7 @@ int upload_we_split(gpp_ctx* c, const HostProblem& h, const HostPins& pins) {
                    c->cstream);
   if (rc) return rc;
   GPP_CUDA(cudaEventRecord(c->ev_we, c->cstream));
-  if (n > 1) {
+  if (real) {
     GPP_CUDA(cudaStreamWaitEvent(c->nstream, c->ev_we, 0));
     GPP_NCCL(ncclGroupStart());
     for (int r = 0; r < n; ++r) {
