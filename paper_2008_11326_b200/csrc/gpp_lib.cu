@@ -1081,15 +1081,18 @@ bool host_pinned(const void* p) {
 }
 
 // Host threads that pack pageable inputs into the staging ring:
-// GPP_HOST_THREADS, else the cores this process's share of the node
-// (LOCAL_WORLD_SIZE ranks per node under torchrun), at most 16.
+// GPP_HOST_THREADS, else half the cores of this process's share of the node
+// (LOCAL_WORLD_SIZE ranks per node under torchrun), at most 8 -- the copy
+// saturates PCIe with ~8 (tools/probe_pageable.py: 6.65 ms upload with 8,
+// 6.82 with 16, 8.7 with 4 on a 16-core host), and spinning packers must
+// not starve the thread that issues the copies and kernels.
 int host_threads() {
   static const int n = [] {
     if (const char* e = std::getenv("GPP_HOST_THREADS")) return std::max(1, std::atoi(e));
     int local = 1;
     if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) local = std::max(1, std::atoi(e));
     const int hw = std::max(1, omp_get_num_procs());
-    return std::max(1, std::min(16, hw / local));
+    return std::max(1, std::min(8, hw / local / 2));
   }();
   return n;
 }
