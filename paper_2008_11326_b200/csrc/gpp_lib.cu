@@ -1606,7 +1606,9 @@ int gpp_comm_init(gpp_ctx* c, int nranks, int rank, const unsigned char* id128) 
   }
   c->nranks = nranks;
   c->rank = rank;
-  if (nranks == 1) return GPP_OK;
+  c->comm_aborted = false;
+  // A one-rank communicator is created too (cheap; it exercises the error /
+  // abort path on one GPU); the collectives only run with nranks > 1.
   ncclUniqueId id;
   std::memcpy(&id, id128, sizeof(id));
   GPP_NCCL(ncclCommInitRank(&c->comm, nranks, id, rank));

@@ -683,3 +683,26 @@ def test_factored_kernel_odd_shapes_vs_oracle(dims, nw):
             assert nf == (near, far), variant
     finally:
         ctx.close()
+
+
+def test_error_after_comm_init_aborts_the_communicator():
+    """An error on a rank that holds a communicator aborts it (ncclCommAbort),
+    so its peers fail instead of waiting in a collective it will never join;
+    the context then refuses further work with an NCCL error (a one-rank
+    communicator on one GPU exercises the mechanism)."""
+    from paper_2008_11326_b200.errors import DomainError, GPUError
+    from paper_2008_11326_b200.kernel import comm_unique_id
+
+    p = synth_problem(16, 5, 600, seed=3, nw=3, check=False)
+    ctx = GPPContext(0)
+    try:
+        ctx.comm_init(1, 0, comm_unique_id())
+        ctx.upload(p)
+        ok = ctx.run("rcp_sq", counts=False)[0]
+        assert _bits_equal(ok, evaluate_variant(p, "rcp_sq"))
+        with pytest.raises(DomainError):
+            ctx.upload(p, band_range=(5, 2), force=True)   # bad argument after comm init
+        with pytest.raises(GPUError, match="aborted"):
+            ctx.run("rcp_sq", counts=False)
+    finally:
+        ctx.close()
