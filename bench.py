@@ -627,8 +627,8 @@ def run_ours(args, dist: Dist):
         fres = ctx.run_factored(args.variant, counts=False)[0]
         factored = {"ms": statistics.median(fms),
                     "what": "gpp_run_factored: the reference's factored algorithm (kernel.py:98-114) -- "
-                            "band weights W = aqsntemp conj(aqsmtemp)^T by the repo's FP64 GEMM kernel, "
-                            "then the branch terms; a different algorithm, not a roofline figure"}
+                            "band weights W = aqsntemp conj(aqsmtemp)^T on the FP64 tensor cores (DMMA) fused "
+                            "with the branch terms in one repo kernel; a different algorithm, not a roofline figure"}
         gp = golden_parity(fres, args.workload, args.seed, args.nw) if args.variant == "rcp_sq" else None
         if gp:
             factored["max_rel_err_vs_reference"] = gp["max_rel_err_vs_reference"]

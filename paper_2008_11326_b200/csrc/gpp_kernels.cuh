@@ -1269,19 +1269,26 @@ __global__ void __launch_bounds__(256) gpp_slot_finalize_kernel(
 // the band sum is factored out of the branch terms,
 //     W[ig, igp] = sum_band aqsntemp[ig, band] conj(aqsmtemp[igp, band])
 // (kernel.py:108), then ach[iw] = sum sch[iw, ig, igp] W, asx likewise.
-// One fused kernel: an item is (256-ig block, kFacIgp-igp tile); thread <->
-// ig accumulates its kFacIgp complex W entries over all bands in registers
-// (aqsntemp streamed with a register prefetch ring, the aqsmtemp tile staged
-// in shared memory and read as warp-uniform broadcasts: 4 DFMA per complex
-// multiply-add, FP64 vector pipe), then forms variant V's branch terms per
-// (iw, ig, igp) exactly as PlainPolicy<V> does (kernel.py:63-95) and
-// contracts them with W -- W never goes to memory.  A different algorithm
-// from the per-instance nest (it exploits the band invariance of the
-// reference's wx): time to solution, never a roofline figure.
-// Counts are scaled by nb, the band count W summed over (kernel.py:130-137).
-constexpr int kFacIgp = 8;      // igp per item
-constexpr int kFacChunk = 64;   // aqsmtemp bands staged per pass
-constexpr int kFacDepth = 4;    // aqsntemp bands in flight per thread
+// One fused kernel: an item is (256-ig block, 8-igp tile).  The band GEMM runs
+// on the FP64 tensor cores (DMMA.8x8x4, mma.sync.m8n8k4.f64): warp w owns
+// ig rows [32w, 32w + 32) of the block as four 8x8 (ig x igp) tiles, and a
+// complex multiply-add is four real MMAs (Wr += Ar Br + Ai Bi, Wi += Ai Br -
+// Ar Bi) over 4 bands per step, fragments loaded straight from the
+// column-major arrays (lane (g, q): ig row g, band q; aqsmtemp column g) with
+// a one-step register prefetch.  The epilogue forms variant V's branch terms
+// per (iw, ig, igp) exactly as PlainPolicy<V> does (kernel.py:63-95) for the
+// 4 x 2 (ig, igp) entries of W each lane holds, and contracts them -- W never
+// goes to memory.  A different algorithm from the per-instance nest (it
+// exploits the band invariance of the reference's wx): time to solution,
+// never a roofline figure.  Counts are scaled by nb, the band
+// count W summed over (kernel.py:130-137).
+constexpr int kFacIgp = 8;  // igp per item (one MMA n-tile)
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
 
 template <int V, int NW>
 __global__ void __launch_bounds__(kThreads, 2) gpp_factored_kernel(
@@ -1290,54 +1297,85 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_factored_kernel(
     const double* __restrict__ wx0, int nw_total, int iw0, int ncouls, int ngpown, int nbands,
     int n_igptile, long long n_items, unsigned long long nb_scale, double* partials,
     unsigned long long* cpartials) {
-  __shared__ double2 s_am[kFacChunk][kFacIgp];
   // This thread's ach / asx partials across its items (shared memory, so the
-  // registers stay with the W accumulators).
+  // registers stay with the W fragments).
   __shared__ double s_acc[4 * NW][kThreads];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
 #pragma unroll
   for (int k = 0; k < 4 * NW; ++k) s_acc[k][tid] = 0.0;
   unsigned n_near = 0, n_far = 0;
-  const size_t nc = static_cast<size_t>(ncouls);
+  const size_t nc = static_cast<size_t>(ncouls), ng = static_cast<size_t>(ngpown);
   for (long long item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int igpt = static_cast<int>(item % n_igptile);
     const int igb = static_cast<int>(item / n_igptile);
-    const int ig = igb * kThreads + tid;
-    const bool vig = ig < ncouls;
-    const int igc = vig ? ig : ncouls - 1;
-    double2 W[kFacIgp];
+    const int ig_base = igb * kThreads + warp * 32;
+    // A rows of this lane (clamped: rows past ncouls are masked in the epilogue).
+    const double2* ap[4];
 #pragma unroll
-    for (int j = 0; j < kFacIgp; ++j) W[j] = make_double2(0.0, 0.0);
-    const double2* ap = aqsn + igc;
-    for (int b0 = 0; b0 < nbands; b0 += kFacChunk) {
-      const int nb = min(kFacChunk, nbands - b0);
-      __syncthreads();  // the previous pass's reads of s_am are done
-      for (int k = tid; k < nb * kFacIgp; k += kThreads) {
-        const int bb = k / kFacIgp, j = k - bb * kFacIgp;
-        const int igp = igpt * kFacIgp + j;
-        s_am[bb][j] = igp < ngpown ? __ldg(aqsm + static_cast<size_t>(b0 + bb) * ngpown + igp)
-                                   : make_double2(0.0, 0.0);
+    for (int s = 0; s < 4; ++s) ap[s] = aqsn + min(ig_base + 8 * s + g, ncouls - 1);
+    const double2* bp = aqsm + min(igpt * kFacIgp + g, ngpown - 1);
+    double wr[4][2], wi[4][2];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) wr[s][0] = wr[s][1] = wi[s][0] = wi[s][1] = 0.0;
+    // Band step k0: this lane's band is k0 + q (zero past nbands).  The main
+    // loop runs while the prefetched step is whole (no guards); the last
+    // one or two steps take the guarded path.
+    const double2* pa[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) pa[s] = ap[s] + q * nc;
+    const double2* pb = bp + q * ng;
+    const size_t sa = 4 * nc, sb = 4 * ng;
+    double2 a_cur[4], b_cur;
+    {
+      const bool v = q < nbands;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) a_cur[s] = v ? __ldg(pa[s]) : make_double2(0.0, 0.0);
+      b_cur = v ? __ldg(pb) : make_double2(0.0, 0.0);
+    }
+    int k0 = 0;
+    for (; k0 + 8 <= nbands; k0 += 4) {
+      double2 a_nxt[4];
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        pa[s] += sa;
+        a_nxt[s] = __ldg(pa[s]);
       }
-      __syncthreads();
-      double2 ring[kFacDepth];
+      pb += sb;
+      const double2 b_nxt = __ldg(pb);
+      const double nbi = -b_cur.y;
 #pragma unroll
-      for (int s = 0; s < kFacDepth; ++s)
-        ring[s] = s < nb ? __ldg(ap + static_cast<size_t>(b0 + s) * nc) : make_double2(0.0, 0.0);
-      for (int bb = 0; bb < nb; bb += kFacDepth) {
-#pragma unroll
-        for (int s = 0; s < kFacDepth; ++s) {
-          const double2 an = ring[s];
-          if (bb + s + kFacDepth < nb) ring[s] = __ldg(ap + static_cast<size_t>(b0 + bb + s + kFacDepth) * nc);
-          if (bb + s < nb) {
-#pragma unroll
-            for (int j = 0; j < kFacIgp; ++j) {
-              const double2 am = s_am[bb + s][j];
-              W[j].x = fma(an.x, am.x, fma(an.y, am.y, W[j].x));   // an * conj(am)
-              W[j].y = fma(an.y, am.x, fma(-an.x, am.y, W[j].y));
-            }
-          }
-        }
+      for (int s = 0; s < 4; ++s) {
+        dmma(wr[s], a_cur[s].x, b_cur.x);   // Ar Br
+        dmma(wr[s], a_cur[s].y, b_cur.y);   // + Ai Bi
+        dmma(wi[s], a_cur[s].y, b_cur.x);   // Ai Br
+        dmma(wi[s], a_cur[s].x, nbi);       // - Ar Bi
       }
+#pragma unroll
+      for (int s = 0; s < 4; ++s) a_cur[s] = a_nxt[s];
+      b_cur = b_nxt;
+    }
+    for (; k0 < nbands; k0 += 4) {
+      double2 a_nxt[4], b_nxt;
+      const bool vn = k0 + 4 + q < nbands;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        pa[s] += sa;
+        a_nxt[s] = vn ? __ldg(pa[s]) : make_double2(0.0, 0.0);
+      }
+      pb += sb;
+      b_nxt = vn ? __ldg(pb) : make_double2(0.0, 0.0);
+      const double nbi = -b_cur.y;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        dmma(wr[s], a_cur[s].x, b_cur.x);
+        dmma(wr[s], a_cur[s].y, b_cur.y);
+        dmma(wi[s], a_cur[s].y, b_cur.x);
+        dmma(wi[s], a_cur[s].x, nbi);
+      }
+#pragma unroll
+      for (int s = 0; s < 4; ++s) a_cur[s] = a_nxt[s];
+      b_cur = b_nxt;
     }
     Acc<NW> acc;
 #pragma unroll
@@ -1350,13 +1388,18 @@ __global__ void __launch_bounds__(kThreads, 2) gpp_factored_kernel(
     double wx[NW];
 #pragma unroll
     for (int iw = 0; iw < NW; ++iw) wx[iw] = __ldg(wx0 + iw0 + iw);
+    // Accumulator (s, i): ig = ig_base + 8 s + g, igp = igpt * 8 + 2 q + i.
 #pragma unroll
-    for (int j = 0; j < kFacIgp; ++j) {
-      const int igp = igpt * kFacIgp + j;
-      const bool v = vig && igp < ngpown;
-      const size_t off = static_cast<size_t>(min(igp, ngpown - 1)) * nc + igc;
-      const typename PlainPolicy<V>::St st = PlainPolicy<V>::make(__ldg(wtilde + off), __ldg(eps + off), v);
-      PlainPolicy<V>::template tuple<NW, true, false>(st, W[j].x, W[j].y, wx, acc);
+    for (int s = 0; s < 4; ++s) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int ig = ig_base + 8 * s + g, igp = igpt * kFacIgp + 2 * q + i;
+        const bool v = ig < ncouls && igp < ngpown;
+        const size_t off = static_cast<size_t>(min(igp, ngpown - 1)) * nc + min(ig, ncouls - 1);
+        const typename PlainPolicy<V>::St st =
+            PlainPolicy<V>::make(__ldg(wtilde + off), __ldg(eps + off), v);
+        PlainPolicy<V>::template tuple<NW, true, false>(st, wr[s][i], wi[s][i], wx, acc);
+      }
     }
 #pragma unroll
     for (int iw = 0; iw < NW; ++iw) {
