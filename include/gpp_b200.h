@@ -158,7 +158,7 @@ int gpp_evaluate_host(gpp_ctx* ctx, int32_t variant, int64_t nbands, int64_t ngp
  * production algorithm (rooflab/gpp/kernel.py:98-114) -- the band sum
  * W = aqsntemp conj(aqsmtemp)^T and the contraction of the variant's branch
  * terms per (iw, ig, igp) with W, fused in one hand-written FP64 kernel
- * (gpp_factored_kernel; W stays in registers).  Only valid for a band-invariant
+ * (gpp_factored_kernel: the GEMM on the DMMA tensor cores, W stays in registers).  Only valid for a band-invariant
  * wx (GPP_ERR_ARG otherwise).  A different algorithm from the per-instance
  * nest gpp_run evaluates: time to solution, not a roofline figure.  With a
  * communicator attached the partials are all-reduced as in gpp_run. */
