@@ -69,7 +69,32 @@ NCU_METRICS = (
     "dram__bytes_write.sum",
     "gpu__time_duration.sum",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "l1tex__t_bytes.sum",
+    "lts__t_bytes.sum",
+    "dram__bytes.sum",
 )
+# The reference's profiler-CSV columns (rooflab/metrics.py:228-237,
+# DEFAULT_PROFILER_MAPPING): the live capture is also written in that form.
+ROOFLAB_COLUMNS = {
+    "label": "Kernel Name", "runtime": "gpu__time_duration.sum",
+    "dadd": "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
+    "dmul": "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
+    "dfma": "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
+    "l1": "l1tex__t_bytes.sum", "l2": "lts__t_bytes.sum", "hbm": "dram__bytes.sum",
+}
+
+
+def rooflab_csv(record: dict, path: Path) -> None:
+    """One evaluation's production-kernel counters as a CSV that the
+    reference's import_profiler_csv reads with its default mapping
+    (runtime in seconds: runtime_scale=1)."""
+    cols = list(ROOFLAB_COLUMNS.values())
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(cols)
+        c, b = record["counters"], record["bytes"]
+        w.writerow([record["label"], record["runtime"], c["dadd"], c["dmul"], c["dfma"],
+                    b["l1"], b["l2"], b["hbm"]])
 
 
 def parse_args():
@@ -389,7 +414,19 @@ def ncu_capture(args, timeout_s: float = 420.0) -> dict | None:
     dadd = sum(val(r, NCU_METRICS[2]) for r in main)
     dur = sum(val(r, "gpu__time_duration.sum") for r in main)
     pipe = (sum(val(r, NCU_METRICS[6]) * val(r, "gpu__time_duration.sum") for r in main) / dur) if dur else None
+    # KernelMetrics-shaped record (rooflab/metrics.py:110-217) of the whole
+    # evaluation's production-kernel launches, in the reference's units.
+    record = {
+        "label": f"gpp_sacc_kernel {dims_of(args)} nw{args.nw} x{args.gpus} shards",
+        "runtime": dur * 1e-9,
+        "counters": {"dadd": int(dadd), "dmul": int(dmul), "dfma": int(dfma), "ddiv": 0, "dother": 0},
+        "bytes": {k: sum(val(r, ROOFLAB_COLUMNS[k]) for r in main) for k in ("l1", "l2", "hbm")},
+        "system": "B200",
+    }
+    if os.environ.get("GPP_ROOFLAB_CSV"):
+        rooflab_csv(record, Path(os.environ["GPP_ROOFLAB_CSV"]))
     return {
+        "rooflab_record": record,
         "source": f"live ncu capture of this build in this run ({len(main)} production-kernel + "
                   f"{len(fin)} finalize launches, --clock-control none, {time.perf_counter() - t0:.0f} s)",
         "lib_sha256": lib_sha256(),
