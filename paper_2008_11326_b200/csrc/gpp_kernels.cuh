@@ -38,6 +38,9 @@ namespace gpp {
 
 constexpr int kThreads = 256;     // threads per CTA (= ig per item)
 constexpr int kMaxChunk = 128;    // bands per item (upper bound)
+#ifndef GPP_ABL
+#define GPP_ABL 0  // timing ablations (tools/ablate.sh); 0 in every real build
+#endif
 #ifndef GPP_SACC_CHUNK
 #define GPP_SACC_CHUNK 256
 #endif
@@ -781,6 +784,9 @@ __device__ __forceinline__ void sacc_band(const double2 an, const double2 (&am)[
             "mov.b64 {rl, rh}, s;\n\t"
             "mov.b64 %0, {wl, rh};\n\t}"
             : "=d"(r) : "d"(wdre), "d"(d));
+#if GPP_ABL & 4
+        r = d;  // ablation: no MUFU seed dependency
+#endif
         const double t = d * r;
         const double e = fma(-t, r, 1.0);
         const double pe = fma(e, 0.375, 0.5);
@@ -805,6 +811,10 @@ __device__ __forceinline__ void sacc_band(const double2 an, const double2 (&am)[
             "mov.b64 %1, {gl, gh};\n\t}"
             : "=d"(in), "=d"(gf)
             : "l"(__double_as_longlong(d)), "l"(qbits), "d"(inv), "d"(sq));
+#if GPP_ABL & 1  // ablation: no branch selection
+        in = inv;
+        gf = sq;
+#endif
 #ifdef GPP_EXACT_SELECT  // A/B reference build (tools/ab_select.sh): full 64-bit selects
         asm("{\n\t.reg .pred pn;\n\t"
             "setp.gt.s64 pn, %2, %3;\n\t"
@@ -826,8 +836,10 @@ __device__ __forceinline__ void sacc_band(const double2 an, const double2 (&am)[
       S1[j][iw].y = fma(s1, ti, S1[j][iw].y);
       S2[j][iw].x = fma(in, tr, S2[j][iw].x);
       S2[j][iw].y = fma(in, ti, S2[j][iw].y);
+#if !(GPP_ABL & 2)  // ablation 2: no far-branch accumulation
       Sf[j][iw].x = fma(gf, tr, Sf[j][iw].x);
       Sf[j][iw].y = fma(gf, ti, Sf[j][iw].y);
+#endif
     }
   }
 }
