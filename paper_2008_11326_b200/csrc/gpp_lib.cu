@@ -1507,8 +1507,9 @@ static int gpp_time_impl(gpp_ctx* c, int32_t variant, int32_t iters, float* tota
       result = enqueue_eval(c, variant, false, &evs[2 * static_cast<size_t>(i)], true);
     if (result) break;
     e = cudaEventRecord(c->ev[3], c->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    if (e != cudaSuccess) { result = cuda_fail(e, "gpp_time sync"); break; }
+    if (e != cudaSuccess) { result = cuda_fail(e, "gpp_time record"); break; }
+    result = wait_stream(c, c->stream);  // polls the communicator's health
+    if (result) break;
     float tot = 0.f, mm = 0.f;
     cudaEventElapsedTime(&tot, c->ev[2], c->ev[3]);
     for (int i = 0; i < iters; ++i) {
