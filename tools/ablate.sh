@@ -19,13 +19,15 @@ if [ "$1" = build ]; then
   ls -la $OUT
 else
   for r in 1 2; do
-    for a in 0 1 2 4 3 7; do
+    for a in ${ABL_SET:-0 1 2 4 3 7}; do
       GPP_B200_LIB=$OUT/abl$a.so python -c "
 import sys; sys.path.insert(0, '.')
 from paper_2008_11326_b200 import GPPContext
-c = GPPContext(0); c.synth(512, 66, 32768, seed=1, nw=3)
-c.time('rcp_sq', 3); tot, main = c.time('rcp_sq', 20)
-print('GPP_ABL=$a', f'{main / 20:.4f} ms')"
+c = GPPContext(0)
+for nb, br in ((512, None), (512, (0, 64))):
+    c.synth(nb, 66, 32768, seed=1, nw=3, band_range=br)
+    c.time('rcp_sq', 3); tot, main = c.time('rcp_sq', 20)
+    print('GPP_ABL=$a', 'bands', br or (0, nb), f'{main / 20:.4f} ms')"
     done
   done
 fi
