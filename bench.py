@@ -128,9 +128,19 @@ def dims_of(args) -> tuple[int, int, int]:
 
 
 def lib_sha256() -> str | None:
-    """sha256 of the library's device code (its .nv_fatbin ELF section: the
-    sm_100a kernels ncu counts).  nvcc rebuilds it bit for bit from the same
-    sources, unlike the host part of the .so."""
+    """sha256 of the library's device code as SASS (`cuobjdump -sass`, minus
+    the source-path lines): the sm_100a kernels ncu counts, the same for every
+    build of the same sources.  (The .nv_fatbin bytes are no build
+    fingerprint: -lineinfo's DWARF line table records the sources' mtimes.)
+    Falls back to the .nv_fatbin section when cuobjdump is missing."""
+    try:
+        out = subprocess.run(["cuobjdump", "-sass", str(LIB)], capture_output=True, timeout=120)
+        if out.returncode == 0 and out.stdout:
+            # drop the "identifier = <source path>" lines: the build directory
+            body = b"\n".join(l for l in out.stdout.splitlines() if not l.startswith(b"identifier"))
+            return "sass:" + hashlib.sha256(body).hexdigest()
+    except (OSError, subprocess.TimeoutExpired):
+        pass
     try:
         b = LIB.read_bytes()
         shoff, = struct.unpack_from("<Q", b, 0x28)
@@ -144,6 +154,16 @@ def lib_sha256() -> str | None:
         return None
     except (OSError, struct.error, ValueError, IndexError):
         return None
+
+
+_LIB_SHA = None
+
+
+def lib_sha256_cached() -> str | None:
+    global _LIB_SHA
+    if _LIB_SHA is None:
+        _LIB_SHA = lib_sha256()
+    return _LIB_SHA
 
 
 # ----------------------------------------------------------------------------
@@ -429,7 +449,7 @@ def ncu_capture(args, timeout_s: float = 420.0) -> dict | None:
         "rooflab_record": record,
         "source": f"live ncu capture of this build in this run ({len(main)} production-kernel + "
                   f"{len(fin)} finalize launches, --clock-control none, {time.perf_counter() - t0:.0f} s)",
-        "lib_sha256": lib_sha256(),
+        "lib_sha256": lib_sha256_cached(),
         "executed_flops_main": sum(fl(r) for r in main),
         "executed_flops_all": sum(fl(r) for r in data),
         "per_shard_main_flops": None,
@@ -447,7 +467,7 @@ def committed_capture(args) -> dict | None:
         s = json.loads(NCU_SUMMARY.read_text())
     except (OSError, json.JSONDecodeError):
         return None
-    if s.get("lib_sha256") != lib_sha256():
+    if s.get("lib_sha256") != lib_sha256_cached():
         return None
     key = f"{args.workload}/nw{args.nw}/seed{args.seed}/{args.variant}/shards{args.gpus}"
     w = s.get("workloads", {}).get(key)
@@ -749,7 +769,7 @@ def run_ours(args, dist: Dist):
             "traffic": ((cap or {}).get("dram_bytes_main") / n_ranks) if (cap or {}).get("dram_bytes_main") else None,
             "achieved_kind": "ncu-counted executed FP64 FLOPs of the production kernel per GPU / its CUDA-event time",
             "source": (cap or {}).get("source"),
-            "lib_sha256": lib_sha256(),
+            "lib_sha256": lib_sha256_cached(),
             "peak_source": "measured live: DFMA microbenchmark (gpp_fp64_peak) on this GPU in this run",
             "kernel": "gpp_sacc_kernel (rcp_sq production kernel)",
             "kernel_ms": t_main_ms,
