@@ -183,14 +183,15 @@ int gpp_kernel_info(gpp_ctx* ctx, int32_t variant, int32_t* registers_per_thread
                     int32_t* threads_per_block, int32_t* blocks_per_sm, int32_t* grid,
                     int32_t* igp_tile, int32_t* band_chunk);
 
-/* The production kernel's launch schedule for a whole (unsharded, un-slabbed)
- * evaluation of the first frequency group, with `slots` resident CTAs: pure
- * host logic, no device needed.  Each launch is 6 values: row0, n_rows (rows
- * of (256-ig block, igp tile) pairs), band0, nbands (its band window), bchunk
- * (bands per item) and n_items (items = chunk * n_rows + row - row0, the first
- * n_items of them).  Writes at most max_launches entries; *n_launches is the
- * full count. */
-int gpp_plan(int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw, int32_t slots,
+/* The production kernel's canonical launch schedule for a whole (unsharded,
+ * un-slabbed) evaluation of the first frequency group on a GPU with `sms`
+ * SMs: pure host logic, no device needed.  Each launch is 7 values: row0,
+ * n_rows (rows of (256-ig block, igp tile) pairs), band0, nbands (its band
+ * window), bchunk (bands per item), n_items (items = chunk * n_rows + row -
+ * row0, the first n_items of them) and the igp tile (2-4 igp per thread, the
+ * tile of least padded cost for ngpown; 1 or 2 resident CTAs per SM).
+ * Writes at most max_launches entries; *n_launches is the full count. */
+int gpp_plan(int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw, int32_t sms,
              int32_t max_launches, int32_t* n_launches, int64_t* launches);
 
 /* Number of kernels this context has launched so far (every compute,

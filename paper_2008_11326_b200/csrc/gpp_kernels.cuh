@@ -942,8 +942,18 @@ constexpr size_t sacc_smem_bytes() {
   return sizeof(SaccSmem<NW, IGP_T>);
 }
 
+// Resident CTAs per SM the production kernel is compiled for: two-igp tiles
+// (and the one-frequency kernel) fit 128 registers and run two CTAs per SM;
+// the 3- and 4-igp tiles at nw 2-3 take up to 255 registers and run one CTA
+// (8 warps) per SM -- fewer warps, but 9-12 independent instances per warp
+// and band, and the tuple / ring work amortised over more igp
+// (tools/probe_variants_sweep.py: 1.6-5.5 % faster per column).
+template <int NW, int IGP_T>
+constexpr int sacc_min_blocks() { return (NW >= 2 && IGP_T >= 3) ? 1 : 2; }
+
 template <int NW, int IGP_T, bool COUNT>
-__global__ void __launch_bounds__(kThreads, 2) gpp_sacc_kernel(const __grid_constant__ Params p,
+__global__ void __launch_bounds__(kThreads, (sacc_min_blocks<NW, IGP_T>()))
+    gpp_sacc_kernel(const __grid_constant__ Params p,
                                                                const __grid_constant__ WxTable wxt) {
   extern __shared__ __align__(16) unsigned char sacc_smem_raw[];
   SaccSmem<NW, IGP_T>& sm = *reinterpret_cast<SaccSmem<NW, IGP_T>*>(sacc_smem_raw);

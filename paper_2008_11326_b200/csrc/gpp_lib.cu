@@ -300,7 +300,28 @@ KernelFn pick_plain(int nw) {
 // do not fit beside the ach/asx shared-memory slab.
 int sacc_cap(int nw) { return nw >= 2 ? gpp::sacc_cap<3>() : gpp::sacc_cap<1>(); }
 
-int sacc_igp(int nw) { return nw <= 1 ? 3 : 2; }
+// The production kernel's igp tile for a frequency group of nw and a problem
+// of ngpown igp columns: the tile of least padded cost, ceil(ngpown / T) * T
+// columns weighted by the measured per-column time of each instantiation
+// relative to the two-igp tile (tools/probe_variants_sweep.py, all 24 sweep
+// points at nw 2 and 3): nw 3: T = 3 x 0.984, T = 4 x 0.980 (one CTA per SM);
+// nw 2: T = 3 x 0.985, T = 4 x 0.945.  One frequency keeps T = 3 (two CTAs
+// per SM; one CTA per SM measured 4 % slower).  The rule picks the fastest
+// measured tile at every sweep point.
+int sacc_igp(int nw, int64_t ngpown) {
+  if (nw <= 1) return 3;
+  const double w3 = nw >= 3 ? 0.984 : 0.985, w4 = nw >= 3 ? 0.980 : 0.945;
+  const double c2 = static_cast<double>((ngpown + 1) / 2 * 2);
+  const double c3 = w3 * static_cast<double>((ngpown + 2) / 3 * 3);
+  const double c4 = w4 * static_cast<double>((ngpown + 3) / 4 * 4);
+  if (c4 <= c3 && c4 < c2) return 4;
+  if (c3 < c2) return 3;
+  return 2;
+}
+
+// Resident CTAs per SM of the production kernel for (nw, igp tile), as its
+// launch bounds declare (the occupancy API confirms it at plan time).
+int sacc_blocks_per_sm(int nw, int igp_t) { return (nw >= 2 && igp_t >= 3) ? 1 : 2; }
 
 template <int NW, int IGP_T, bool C>
 KernelRef sacc_ref() {
@@ -311,11 +332,13 @@ KernelRef sacc_ref() {
 }
 
 template <bool C>
-KernelRef pick_sacc(int nw) {
+KernelRef pick_sacc(int nw, int igp_t) {
   switch (nw) {
     case 1: return sacc_ref<1, 3, C>();
-    case 2: return sacc_ref<2, 2, C>();
-    case 3: return sacc_ref<3, 2, C>();
+    case 2:
+      return igp_t == 4 ? sacc_ref<2, 4, C>() : igp_t == 3 ? sacc_ref<2, 3, C>() : sacc_ref<2, 2, C>();
+    case 3:
+      return igp_t == 4 ? sacc_ref<3, 4, C>() : igp_t == 3 ? sacc_ref<3, 3, C>() : sacc_ref<3, 2, C>();
     default: {
       KernelRef k;
       k.fn = gpp::gpp_main_kernel<gpp::FastPolicy, 4, 3, C>;
@@ -333,7 +356,7 @@ KernelRef pick_kernel_c(int variant, int nw, int igp_t) {
     case GPP_KERNEL_SQ_SPLIT: k.fn = pick_fast_nw<gpp::FastPolicyT<0, 2>, C>(nw, igp_t); break;
     case GPP_KERNEL_IW_HOIST: k.fn = pick_fast_nw<gpp::FastPolicyT<1, 3>, C>(nw, igp_t); break;
     case GPP_KERNEL_ONE_SEED: k.fn = pick_fast_nw<gpp::FastPolicy, C>(nw, igp_t); break;
-    default: k = pick_sacc<C>(nw); break;
+    default: k = pick_sacc<C>(nw, igp_t); break;
   }
   return k;
 }
@@ -434,7 +457,7 @@ int make_plan_uncached(gpp_ctx* c, int variant, int nw_group, bool count, Plan* 
   if (variant == GPP_VARIANT_DIV || variant == GPP_VARIANT_RCP)
     pl->igp_t = 2;  // the only instantiation of the plain kernels
   else if (variant == GPP_VARIANT_RCP_SQ)
-    pl->igp_t = sacc_igp(nw_group);
+    pl->igp_t = sacc_igp(nw_group, c->ngpown);
   else
     pl->igp_t = fast_igp(nw_group, tune.igp >= 2 && tune.igp <= 4 ? tune.igp
                                                                   : choose_igp_tile(c->ngpown));
@@ -1524,13 +1547,14 @@ static int gpp_time_impl(gpp_ctx* c, int32_t variant, int32_t iters, float* tota
   return result;
 }
 
-int gpp_plan(int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw, int32_t slots,
+int gpp_plan(int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw, int32_t sms,
              int32_t max_launches, int32_t* n_launches, int64_t* launches) {
-  if (nbands < 1 || ngpown < 1 || ncouls < 1 || nw < 1 || slots < 1 || !n_launches ||
+  if (nbands < 1 || ngpown < 1 || ncouls < 1 || nw < 1 || sms < 1 || !n_launches ||
       (max_launches > 0 && !launches))
     return fail(GPP_ERR_ARG, "gpp_plan: bad argument");
   const int nwg = std::min<int>(nw, max_group(GPP_VARIANT_RCP_SQ));
-  const int igp_t = sacc_igp(nwg);
+  const int igp_t = sacc_igp(nwg, ngpown);
+  const long long slots = static_cast<long long>(sms) * sacc_blocks_per_sm(nwg, igp_t);
   const int n_igblk = static_cast<int>((ncouls + gpp::kThreads - 1) / gpp::kThreads);
   const int n_igptile = static_cast<int>((ngpown + igp_t - 1) / igp_t);
   const int plan_bchunk = choose_bchunk(n_igblk, n_igptile, nbands, slots, sacc_cap(nwg),
@@ -1541,13 +1565,14 @@ int gpp_plan(int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw, int32_t
   *n_launches = static_cast<int32_t>(all.size());
   for (int32_t k = 0; k < std::min<int32_t>(max_launches, *n_launches); ++k) {
     const CanonLaunch& L = all[k];
-    int64_t* o = launches + 6 * k;
+    int64_t* o = launches + 7 * k;
     o[0] = L.row0;
     o[1] = L.n_rows;
     o[2] = L.wb0;
     o[3] = L.wnb;
     o[4] = L.bchunk;
     o[5] = L.n_items;
+    o[6] = igp_t;
   }
   return GPP_OK;
 }

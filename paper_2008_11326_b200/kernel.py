@@ -398,17 +398,18 @@ def evaluate_factored(problem, variant: str = "rcp_sq", device: int = 0) -> GPPR
         return ctx.run_factored(variant, counts=False)[0]
 
 
-def plan_schedule(nbands: int, ngpown: int, ncouls: int, nw: int, slots: int = 296) -> list[dict]:
-    """The production kernel's launches for a whole evaluation (first
-    frequency group) with ``slots`` resident CTAs (gpp_plan; host logic only,
-    no GPU needed): band windows, whole-wave launches and balanced tails."""
+def plan_schedule(nbands: int, ngpown: int, ncouls: int, nw: int, sms: int = 148) -> list[dict]:
+    """The production kernel's canonical launches for a whole evaluation
+    (first frequency group) on a GPU with ``sms`` SMs (gpp_plan; host logic
+    only, no GPU needed): band windows, whole-wave launches and balanced
+    tails, and the igp tile chosen for ngpown."""
     lib = _lib.load()
     n = ctypes.c_int32(0)
-    _lib.check(lib.gpp_plan(nbands, ngpown, ncouls, nw, slots, 0, ctypes.byref(n), None), "gpp_plan")
-    out = np.zeros((max(n.value, 1), 6), dtype=np.int64)
-    _lib.check(lib.gpp_plan(nbands, ngpown, ncouls, nw, slots, n.value, ctypes.byref(n),
+    _lib.check(lib.gpp_plan(nbands, ngpown, ncouls, nw, sms, 0, ctypes.byref(n), None), "gpp_plan")
+    out = np.zeros((max(n.value, 1), 7), dtype=np.int64)
+    _lib.check(lib.gpp_plan(nbands, ngpown, ncouls, nw, sms, n.value, ctypes.byref(n),
                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))), "gpp_plan")
-    keys = ("row0", "n_rows", "band0", "nbands", "bchunk", "n_items")
+    keys = ("row0", "n_rows", "band0", "nbands", "bchunk", "n_items", "igp_tile")
     return [dict(zip(keys, (int(v) for v in row))) for row in out[: n.value]]
 
 

@@ -13,13 +13,12 @@ from paper_2008_11326_b200.kernel import plan_schedule
 K_WX_PARAM = 1536
 
 
-def _igp_tile(nw: int) -> int:
-    return 3 if nw == 1 else 2
-
-
-def _coverage(nbands, ngpown, ncouls, nw, slots):
-    plan = plan_schedule(nbands, ngpown, ncouls, nw, slots)
-    n_rows = -(-ncouls // 256) * -(-ngpown // _igp_tile(nw))
+def _coverage(nbands, ngpown, ncouls, nw, sms):
+    plan = plan_schedule(nbands, ngpown, ncouls, nw, sms)
+    igp_tile = plan[0]["igp_tile"]
+    assert all(L["igp_tile"] == igp_tile for L in plan)
+    assert igp_tile == 3 if nw == 1 else igp_tile in (2, 3, 4)
+    n_rows = -(-ncouls // 256) * -(-ngpown // igp_tile)
     cov = np.zeros((n_rows, nbands), dtype=np.int32)
     for L in plan:
         assert 0 <= L["band0"] and L["band0"] + L["nbands"] <= nbands
@@ -37,30 +36,42 @@ def _coverage(nbands, ngpown, ncouls, nw, slots):
 
 
 def test_paper_size_schedule():
-    """(512, 66, 32768) at nw 3 on 296 resident CTAs: 14 whole waves of
-    512-band items (one per (igb, igp tile) row), then the last wave's 80
-    rows in 47-band chunks."""
-    plan = plan_schedule(512, 66, 32768, 3, 296)
+    """(512, 66, 32768) at nw 3 on 148 SMs: 3-igp tiles (no padding, one CTA
+    per SM: 148 resident CTAs), 19 whole waves of 512-band items (one per
+    (igb, igp tile) row), then the last wave's 4 rows in 14-band chunks."""
+    plan = plan_schedule(512, 66, 32768, 3, 148)
     assert plan == [
-        {"row0": 0, "n_rows": 4224, "band0": 0, "nbands": 512, "bchunk": 512, "n_items": 14 * 296},
-        {"row0": 4224 - 80, "n_rows": 80, "band0": 0, "nbands": 512, "bchunk": 47,
-         "n_items": 80 * 11},
+        {"row0": 0, "n_rows": 2816, "band0": 0, "nbands": 512, "bchunk": 512, "n_items": 19 * 148,
+         "igp_tile": 3},
+        {"row0": 2816 - 4, "n_rows": 4, "band0": 0, "nbands": 512, "bchunk": 14, "n_items": 4 * 37,
+         "igp_tile": 3},
     ]
 
 
-@pytest.mark.parametrize("dims,nw,slots", [
-    ((512, 66, 32768), 3, 296),
-    ((64, 66, 32768), 3, 296),     # 8-way band shard of the paper size
-    ((600, 7, 5000), 3, 296),      # two band windows
-    ((1100, 5, 3000), 2, 296),
-    ((1600, 4, 2000), 1, 296),
-    ((258, 33, 8192), 3, 296),     # 2-band last chunk
-    ((5, 7, 70000), 3, 296),
-    ((1, 1, 1), 3, 296),
-    ((300, 9, 20000), 2, 100),     # other SM counts
+@pytest.mark.parametrize("ngpown,nw,tile", [
+    (16, 3, 4), (33, 3, 3), (66, 3, 3), (132, 3, 4), (264, 3, 4), (528, 3, 4),
+    (16, 2, 4), (33, 2, 3), (66, 2, 4), (528, 2, 4), (5, 2, 3), (7, 3, 4), (1, 3, 2), (66, 1, 3),
 ])
-def test_every_instance_is_scheduled_exactly_once(dims, nw, slots):
-    _, cov = _coverage(*dims, nw, slots)
+def test_igp_tile_choice(ngpown, nw, tile):
+    """The production kernel's igp tile: least padded cost, weighted by the
+    measured per-column time of each instantiation (tools/probe_variants_sweep.py
+    picks the same tile at every sweep point)."""
+    assert plan_schedule(512, ngpown, 8192, nw, 148)[0]["igp_tile"] == tile
+
+
+@pytest.mark.parametrize("dims,nw,sms", [
+    ((512, 66, 32768), 3, 148),
+    ((64, 66, 32768), 3, 148),     # 8-way band shard of the paper size
+    ((600, 7, 5000), 3, 148),      # two band windows
+    ((1100, 5, 3000), 2, 148),
+    ((1600, 4, 2000), 1, 148),
+    ((258, 33, 8192), 3, 148),     # 2-band last chunk
+    ((5, 7, 70000), 3, 148),
+    ((1, 1, 1), 3, 148),
+    ((300, 9, 20000), 2, 50),      # other SM counts
+])
+def test_every_instance_is_scheduled_exactly_once(dims, nw, sms):
+    _, cov = _coverage(*dims, nw, sms)
     assert cov.min() == 1 and cov.max() == 1
 
 
@@ -71,13 +82,13 @@ def test_random_schedules_cover_exactly_once():
         ngpown = int(rng.integers(1, 40))
         ncouls = int(rng.integers(1, 20000))
         nw = int(rng.integers(1, 5))
-        slots = int(rng.integers(1, 400))
-        _, cov = _coverage(nbands, ngpown, ncouls, nw, slots)
-        assert cov.min() == 1 and cov.max() == 1, (nbands, ngpown, ncouls, nw, slots)
+        sms = int(rng.integers(1, 200))
+        _, cov = _coverage(nbands, ngpown, ncouls, nw, sms)
+        assert cov.min() == 1 and cov.max() == 1, (nbands, ngpown, ncouls, nw, sms)
 
 
 def test_tail_only_when_it_shortens_the_modelled_makespan():
     # A problem whose items are an exact multiple of the resident CTAs has
     # no partial wave, hence no tail launch.
-    plan = plan_schedule(256, 2, 296 * 256, 3, 296)
-    assert len(plan) == 1 and plan[0]["n_items"] % 296 == 0
+    plan = plan_schedule(256, 2, 296 * 256, 3, 148)
+    assert plan[0]["igp_tile"] == 2 and len(plan) == 1 and plan[0]["n_items"] % 296 == 0
