@@ -1315,26 +1315,24 @@ std::vector<int> slab_schedule(gpp_ctx* c, const EvalRun& r, int n_blk, int slab
                                     cn.pl.n_igptile;
       tail_blocks = std::max(0, tail_blocks / cn.pl.n_igptile);
     }
-    // Built from the end: the tail blocks, then growing slabs.  Pinned
-    // inputs: by ~1.25x up to two waves of rows (tools/probe_slabs3.py: 6.57
-    // ms end to end at the paper size against 6.72-7.0 ms for equal slabs of
-    // 4-16 blocks).  Pageable inputs (packed into the staging ring, where
-    // narrow slabs pack slowly): doubling up to one wave, then +1 wave up to
-    // five (tools/probe_pageable3.py: 7.0-7.2 ms against 7.5 for the taper).
+    // Built from the end: a last slab of max(2, tail) blocks, then slabs of
+    // 1, 2, 3, ... waves of rows (resident CTAs / igp tiles blocks), the
+    // first slab taking the remainder: every slab's items keep pace with the
+    // copy of the next one, and little work follows the last byte
+    // (tools/probe_slabs4.py: 6.66 ms pinned / 7.23 ms pageable at the paper
+    // size against 6.74-6.90 / 8.2-8.7 for equal slabs of 1-2 waves).
     std::vector<int> rev;
-    int sum = 0, sz = std::max(1, tail_blocks);
-    if (tail_blocks <= 0 || tail_blocks >= n_blk) sz = 1;
-    bool first = true;
+    int sum = 0, k = 1;
+    const int last = std::min(n_blk, std::max(2, tail_blocks));
+    rev.push_back(last);
+    sum = last;
     while (sum < n_blk) {
-      const int take = std::min(sz, n_blk - sum);
+      const int take = std::min(k * per, n_blk - sum);
       rev.push_back(take);
       sum += take;
-      if (pageable)
-        sz = first ? sz : std::min(5 * per, sz < per ? 2 * sz : sz + per);
-      else
-        sz = std::min(2 * per, std::max(sz + 1, static_cast<int>(std::ceil(sz * 1.25))));
-      first = false;
+      ++k;
     }
+    (void)pageable;
     sizes.assign(rev.rbegin(), rev.rend());
   }
   std::vector<int> blk0{0};
