@@ -950,9 +950,36 @@ constexpr size_t sacc_smem_bytes() {
 // (tools/probe_variants_sweep.py: 1.6-5.5 % faster per column).
 template <int NW, int IGP_T>
 constexpr int sacc_min_blocks() { return (NW >= 2 && IGP_T >= 3) ? 1 : 2; }
+// Register budget per instantiation: 128 for two CTAs per SM; for the
+// one-CTA tiles the cap that measured fastest over the aspect-ratio sweep
+// (tools/probe_variants_sweep.py over builds with GPP_R<nw><igp>): a cap
+// below 255 changes ptxas's schedule (and whether wx stays on the uniform
+// datapath): nw 3 / 4-igp at 240: 1.1-1.6 % faster than at 255; nw 2 /
+// 3-igp at 184: 2 % faster; the others fastest at 255 (the RF model's
+// predicted gains for caps on the 3-igp nw-3 tile did not materialise).
+#ifndef GPP_R33
+#define GPP_R33 255
+#endif
+#ifndef GPP_R34
+#define GPP_R34 240
+#endif
+#ifndef GPP_R23
+#define GPP_R23 184
+#endif
+#ifndef GPP_R24
+#define GPP_R24 255
+#endif
+template <int NW, int IGP_T>
+constexpr int sacc_maxnreg() {
+  return sacc_min_blocks<NW, IGP_T>() == 2 ? 128
+         : (NW == 3 && IGP_T == 3)         ? GPP_R33
+         : (NW == 3 && IGP_T == 4)         ? GPP_R34
+         : (NW == 2 && IGP_T == 3)         ? GPP_R23
+                                           : GPP_R24;
+}
 
 template <int NW, int IGP_T, bool COUNT>
-__global__ void __launch_bounds__(kThreads, (sacc_min_blocks<NW, IGP_T>()))
+__global__ void __maxnreg__((sacc_maxnreg<NW, IGP_T>()))
     gpp_sacc_kernel(const __grid_constant__ Params p,
                                                                const __grid_constant__ WxTable wxt) {
   extern __shared__ __align__(16) unsigned char sacc_smem_raw[];
