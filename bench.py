@@ -224,6 +224,16 @@ class Dist:
 # ----------------------------------------------------------------------------
 # clocks sampler: NVML every 5 ms during the timed region (nvidia-smi fallback)
 # ----------------------------------------------------------------------------
+def nvml_devices(n: int) -> list[int]:
+    """NVML indices of the first n CUDA devices (CUDA_VISIBLE_DEVICES order
+    when it lists plain indices)."""
+    cvd = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+    ids = [x.strip() for x in cvd.split(",") if x.strip()]
+    if ids and all(x.isdigit() for x in ids):
+        return [int(x) for x in ids[:n]]
+    return list(range(n))
+
+
 class Clocks:
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4}
@@ -596,7 +606,7 @@ def run_ours(args, dist: Dist):
     bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
     for attempt in range(2):  # a run that saw a slowdown reason is re-measured once
         dist.barrier()
-        clocks = Clocks(list(range(args.gpus)) if dist.rank == 0 else [])
+        clocks = Clocks(nvml_devices(args.gpus) if dist.rank == 0 else [])
         clocks.start()
         l0 = launches()
         total_ms, main_ms = timed(args.steps)
