@@ -154,10 +154,10 @@ struct gpp_ctx {
 
   // Pinned staging ring for pageable host inputs (copy_rows): kStageSlots
   // buffers of stage_cap bytes; slot k is free once stage_ev[k] completed.
-  static constexpr int kStageSlots = 4;
-  unsigned char* h_stage[kStageSlots] = {nullptr, nullptr, nullptr, nullptr};
+  static constexpr int kStageSlots = 16;  // capacity; stage_slots() in use
+  unsigned char* h_stage[kStageSlots] = {};
   size_t stage_cap = 0;
-  cudaEvent_t stage_ev[kStageSlots] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t stage_ev[kStageSlots] = {};
   int stage_next = 0;
   uint64_t staged_bytes = 0;  // bytes that went through the staging ring (gpp_stats)
 
@@ -1130,9 +1130,18 @@ size_t stage_bytes() {
   return n;
 }
 
+// Staging buffers in the ring: 4 (GPP_STAGE_SLOTS overrides, <= 16).
+int stage_slots() {
+  static const int n = [] {
+    const char* e = std::getenv("GPP_STAGE_SLOTS");
+    return e ? std::max(2, std::min(gpp_ctx::kStageSlots, std::atoi(e))) : 4;
+  }();
+  return n;
+}
+
 int ensure_stage(gpp_ctx* c) {
   if (c->stage_cap >= stage_bytes()) return GPP_OK;
-  for (int k = 0; k < gpp_ctx::kStageSlots; ++k) {
+  for (int k = 0; k < stage_slots(); ++k) {
     if (c->h_stage[k]) {
       if (c->stage_ev[k]) GPP_CUDA(cudaEventSynchronize(c->stage_ev[k]));
       cudaFreeHost(c->h_stage[k]);
@@ -1168,7 +1177,7 @@ int copy_cols(gpp_ctx* c, double2* dst, const double* src, int64_t ld, int64_t n
   for (int64_t c0 = 0; c0 < ncol; c0 += per) {
     const int64_t c1 = std::min(ncol, c0 + per);
     const int k = c->stage_next;
-    c->stage_next = (k + 1) % gpp_ctx::kStageSlots;
+    c->stage_next = (k + 1) % stage_slots();
     GPP_CUDA(cudaEventSynchronize(c->stage_ev[k]));  // its previous copy has drained
     unsigned char* buf = c->h_stage[k];
     const size_t wbytes = width;
