@@ -308,6 +308,18 @@ def get_context(device: int = 0) -> GPPContext:
     return ctx
 
 
+def release_context(device: int | None = None) -> None:
+    """Free the calling thread's context(s) (device buffers, streams) now
+    instead of at thread exit -- e.g. in long-lived pool threads that are
+    done with a large problem.  ``device=None``: every device."""
+    ctxs = getattr(_TLS, "contexts", None) or {}
+    for d in ([device] if device is not None else list(ctxs)):
+        ctx = ctxs.pop(d, None)
+        if ctx is not None:
+            with ctx.lock:
+                ctx.close()
+
+
 def evaluate(problem, variant: str = "rcp_sq", device: int = 0, counts: bool = True):
     """Upload (cached) + run: (GPPResult, BranchStats | None, kernel_ms).
     The first sight of a problem pipelines its upload with the evaluation

@@ -706,3 +706,18 @@ def test_error_after_comm_init_aborts_the_communicator():
             ctx.run("rcp_sq", counts=False)
     finally:
         ctx.close()
+
+
+def test_release_context_frees_and_recreates():
+    """release_context() drops the calling thread's context; the next call
+    creates a fresh one and returns the same bits."""
+    from paper_2008_11326_b200 import release_context
+    from paper_2008_11326_b200.kernel import get_context
+
+    p = synth_problem(40, 5, 900, seed=6, nw=3, check=False)
+    a = evaluate_variant(p, "rcp_sq")
+    c0 = get_context(0)
+    release_context()
+    c1 = get_context(0)
+    assert c1 is not c0 and not c0._h
+    assert _bits_equal(evaluate_variant(p, "rcp_sq"), a)
