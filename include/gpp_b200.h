@@ -194,6 +194,18 @@ int gpp_kernel_info(gpp_ctx* ctx, int32_t variant, int32_t* registers_per_thread
 int gpp_plan(int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw, int32_t sms,
              int32_t max_launches, int32_t* n_launches, int64_t* launches);
 
+/* The production kernel's launches for one ig slab (256-ig blocks [blk0,
+ * blk1)) of the pipelined evaluate: the canonical items of gpp_plan whose rows
+ * lie in the slab, as sub-launches of 9 values each -- row0, n_rows, band0,
+ * nbands, bchunk, n_items, igp tile, slot_base, slot_stride; item k runs rows
+ * row0 + k % n_rows, band chunk k / n_rows, and writes canonical slot
+ * slot_base + chunk * slot_stride + row.  Pure host logic: the CPU tests
+ * check that any slab partition runs exactly the canonical items, each into
+ * its canonical slot (the basis of the bitwise reproducibility). */
+int gpp_plan_piece(int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw, int32_t sms,
+                   int32_t blk0, int32_t blk1, int32_t max_launches, int32_t* n_launches,
+                   int64_t* launches);
+
 /* Number of kernels this context has launched so far (every compute,
  * finalize, synthesis and factored-path launch): the bench's gpu_launches is
  * the difference across its timed region. */

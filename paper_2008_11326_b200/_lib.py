@@ -70,6 +70,11 @@ SIGNATURES = {
         [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
          ctypes.c_int32, _c_i32_p, _c_i64_p],
     ),
+    "gpp_plan_piece": (
+        ctypes.c_int,
+        [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+         ctypes.c_int32, ctypes.c_int32, _c_i32_p, _c_i64_p],
+    ),
     "gpp_kernel_info": (
         ctypes.c_int,
         [ctypes.c_void_p, ctypes.c_int32, _c_i32_p, _c_i32_p, _c_i32_p, _c_i32_p, _c_i32_p, _c_i32_p],

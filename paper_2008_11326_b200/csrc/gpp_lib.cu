@@ -1584,6 +1584,45 @@ int gpp_plan(int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw, int32_t
   return GPP_OK;
 }
 
+int gpp_plan_piece(int64_t nbands, int64_t ngpown, int64_t ncouls, int32_t nw, int32_t sms,
+                   int32_t blk0, int32_t blk1, int32_t max_launches, int32_t* n_launches,
+                   int64_t* launches) {
+  if (nbands < 1 || ngpown < 1 || ncouls < 1 || nw < 1 || sms < 1 || !n_launches ||
+      (max_launches > 0 && !launches) || blk0 < 0 || blk1 < blk0)
+    return fail(GPP_ERR_ARG, "gpp_plan_piece: bad argument");
+  const int nwg = std::min<int>(nw, max_group(GPP_VARIANT_RCP_SQ));
+  const int igp_t = sacc_igp(nwg, ngpown);
+  const long long slots = static_cast<long long>(sms) * sacc_blocks_per_sm(nwg, igp_t);
+  const int n_igblk = static_cast<int>((ncouls + gpp::kThreads - 1) / gpp::kThreads);
+  const int n_igptile = static_cast<int>((ngpown + igp_t - 1) / igp_t);
+  const int plan_bchunk = choose_bchunk(n_igblk, n_igptile, nbands, slots, sacc_cap(nwg),
+                                       balanced_tail_enabled());
+  long long n_slots = 0;
+  const std::vector<CanonLaunch> all =
+      canon_launches(n_igblk, n_igptile, nbands, nwg, plan_bchunk, slots, &n_slots);
+  const int r0 = std::min(blk0, n_igblk) * n_igptile, r1 = std::min(blk1, n_igblk) * n_igptile;
+  int32_t n = 0;
+  for (const CanonLaunch& C : all) {
+    SaccLaunch L;
+    if (!sub_launch(C, r0, r1, &L)) continue;
+    if (n < max_launches) {
+      int64_t* o = launches + 9 * n;
+      o[0] = L.row0;
+      o[1] = L.n_rows;
+      o[2] = L.wb0;
+      o[3] = L.wnb;
+      o[4] = L.bchunk;
+      o[5] = L.n_items;
+      o[6] = igp_t;
+      o[7] = C.slot0 - C.row0;  // slot_base
+      o[8] = C.n_rows;          // slot_stride
+    }
+    ++n;
+  }
+  *n_launches = n;
+  return GPP_OK;
+}
+
 int gpp_launch_count(gpp_ctx* c, int64_t* launches) {
   CtxLock lock(c);
   if (!c || !launches) return fail(GPP_ERR_ARG, "ctx / launches is NULL");

@@ -425,6 +425,22 @@ def plan_schedule(nbands: int, ngpown: int, ncouls: int, nw: int, sms: int = 148
     return [dict(zip(keys, (int(v) for v in row))) for row in out[: n.value]]
 
 
+def plan_piece(nbands: int, ngpown: int, ncouls: int, nw: int, blk0: int, blk1: int,
+               sms: int = 148) -> list[dict]:
+    """The production kernel's sub-launches for the ig slab [blk0, blk1) of
+    the pipelined evaluate (gpp_plan_piece; host logic only), with the
+    canonical slot mapping of their items."""
+    lib = _lib.load()
+    n = ctypes.c_int32(0)
+    _lib.check(lib.gpp_plan_piece(nbands, ngpown, ncouls, nw, sms, blk0, blk1, 0, ctypes.byref(n), None),
+               "gpp_plan_piece")
+    out = np.zeros((max(n.value, 1), 9), dtype=np.int64)
+    _lib.check(lib.gpp_plan_piece(nbands, ngpown, ncouls, nw, sms, blk0, blk1, n.value, ctypes.byref(n),
+                                  out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))), "gpp_plan_piece")
+    keys = ("row0", "n_rows", "band0", "nbands", "bchunk", "n_items", "igp_tile", "slot_base", "slot_stride")
+    return [dict(zip(keys, (int(v) for v in row))) for row in out[: n.value]]
+
+
 def fp64_peak(device: int = 0, iters: int = 200_000) -> tuple[float, float]:
     """Measured FP64 DFMA throughput of the device: (TFLOP/s, ms)."""
     lib = _lib.load()

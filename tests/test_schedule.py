@@ -92,3 +92,45 @@ def test_tail_only_when_it_shortens_the_modelled_makespan():
     # no partial wave, hence no tail launch.
     plan = plan_schedule(256, 2, 296 * 256, 3, 148)
     assert plan[0]["igp_tile"] == 2 and len(plan) == 1 and plan[0]["n_items"] % 296 == 0
+
+
+def _items(L, slot_of):
+    """(slot -> (row, band0, band1)) of one launch's items."""
+    k = np.arange(L["n_items"])
+    chunk, row = k // L["n_rows"], L["row0"] + k % L["n_rows"]
+    b0 = L["band0"] + chunk * L["bchunk"]
+    b1 = np.minimum(b0 + L["bchunk"], L["band0"] + L["nbands"])
+    return dict(zip(slot_of(chunk, row, k).tolist(), zip(row.tolist(), b0.tolist(), b1.tolist())))
+
+
+def _canonical_items(dims, nw, sms):
+    out, slot0 = {}, 0
+    for L in plan_schedule(*dims, nw, sms):
+        out.update(_items(L, lambda c, r, k, s0=slot0: s0 + k))
+        slot0 += L["n_items"]
+    return out
+
+
+@pytest.mark.parametrize("dims,nw", [((512, 66, 32768), 3), ((64, 66, 32768), 3), ((600, 7, 5000), 3),
+                                     ((1100, 5, 3000), 2), ((300, 10, 3000), 1), ((512, 16, 8192), 3)])
+def test_slab_pieces_run_the_canonical_items(dims, nw):
+    """The basis of bitwise reproducibility: however the ig
+    blocks are cut into slabs for the pipelined evaluate, the slabs' launches
+    run exactly the canonical items -- the same (row, band range) -- each
+    writing its canonical slot, so the slot-order finalize sums the same
+    values in the same order as the resident run."""
+    from paper_2008_11326_b200.kernel import plan_piece
+
+    canon = _canonical_items(dims, nw, 148)
+    n_blk = -(-dims[2] // 256)
+    rng = np.random.default_rng(sum(dims) + nw)
+    for trial in range(4):
+        cuts = sorted(set(rng.integers(1, max(n_blk, 2), size=min(6, n_blk)).tolist()) - {0, n_blk})
+        bounds = [0, *cuts, n_blk] if trial else [0, n_blk]
+        got = {}
+        for b0, b1 in zip(bounds[:-1], bounds[1:]):
+            for L in plan_piece(*dims, nw, b0, b1, 148):
+                items = _items(L, lambda c, r, k, L=L: L["slot_base"] + c * L["slot_stride"] + r)
+                assert not set(items) & set(got), "a slot written twice"
+                got.update(items)
+        assert got == canon, (bounds, len(got), len(canon))
